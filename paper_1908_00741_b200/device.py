@@ -1,0 +1,290 @@
+"""Device plumbing: torch CUDA buffers, streams and the native plan handle.
+
+PyTorch provides device memory and the current stream; every operator is a
+kernel in libhbmc_b200.so called through the C ABI.  Without a CUDA device
+every entry point here raises -- there is no CPU fallback.
+"""
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import LIB, check, ptr
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError(
+            "paper_1908_00741_b200: a CUDA device (B200) is required; this "
+            "operator has no CPU implementation")
+    return t
+
+
+def current_stream():
+    t = require_cuda()
+    return t.cuda.current_stream().cuda_stream
+
+
+def is_cuda_tensor(x):
+    t = torch() if _torch is not None or _has_torch() else None
+    return t is not None and isinstance(x, t.Tensor) and x.is_cuda
+
+
+def _has_torch():
+    try:
+        torch()
+        return True
+    except ImportError:
+        return False
+
+
+def to_device(a, dtype=None):
+    """numpy -> CUDA tensor (contiguous copy)."""
+    t = require_cuda()
+    arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    return t.from_numpy(arr).to("cuda", non_blocking=False)
+
+
+def empty(n, dtype="f64"):
+    t = require_cuda()
+    dt = {"f64": t.float64, "i32": t.int32, "i64": t.int64}[dtype]
+    return t.empty(int(n), dtype=dt, device="cuda")
+
+
+def vec_in(x, n):
+    """Accept numpy or CUDA tensor of length n; returns (tensor, was_numpy)."""
+    t = require_cuda()
+    if isinstance(x, t.Tensor):
+        if not x.is_cuda:
+            x = x.to("cuda")
+        if x.dtype != t.float64:
+            x = x.to(t.float64)
+        x = x.contiguous()
+        if x.shape[0] != n:
+            raise ValueError(f"vector length {x.shape[0]}, expected {n}")
+        return x, False
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if a.shape[0] != n:
+        raise ValueError(f"vector length {a.shape[0]}, expected {n}")
+    return to_device(a), True
+
+
+def vec_out(tensor, as_numpy):
+    if as_numpy:
+        return tensor.cpu().numpy()
+    return tensor
+
+
+# ------------------------------------------------------------------ matrices
+class DeviceSell:
+    """Device copy of a SellMatrix (int32 columns)."""
+
+    def __init__(self, s):
+        self.n_slices = s.n_slices
+        self.width = s.width
+        self.n = s.n
+        self.n_pad = s.n_pad
+        self.slice_ptr = to_device(s.slice_ptr, np.int64)
+        self.slice_len = to_device(s.slice_len, np.int32)
+        self.col = to_device(s.col32, np.int32)
+        self.vals = to_device(s.vals, np.float64)
+
+
+class DeviceCsr:
+    def __init__(self, a):
+        self.n = a.n
+        self.row_ptr = to_device(a.row_ptr, np.int64)
+        self.col = to_device(a.col_idx, np.int32)
+        self.vals = to_device(a.vals, np.float64)
+
+
+def device_copy(obj):
+    """Cached device copy of a (never mutated) CsrMatrix / SellMatrix."""
+    from .matrix import CsrMatrix, SellMatrix
+    dev = getattr(obj, "_tb_dev", None)
+    if dev is None:
+        if isinstance(obj, SellMatrix):
+            dev = DeviceSell(obj)
+        elif isinstance(obj, CsrMatrix):
+            dev = DeviceCsr(obj)
+        else:
+            raise TypeError(f"spmv: unsupported matrix type {type(obj).__name__}")
+        object.__setattr__(obj, "_tb_dev", dev)
+    return dev
+
+
+def spmv(a, x):
+    """src/matrix.py:307-323 on the device."""
+    from .matrix import CsrMatrix, SellMatrix
+    t = require_cuda()
+    if isinstance(a, SellMatrix):
+        xt, was_np = vec_in_pad(x, a.n_pad)
+        d = device_copy(a)
+        out = empty(a.n_pad)
+        check(LIB.tb_dev_spmv_sell(d.n_slices, ptr(d.slice_ptr), ptr(d.slice_len),
+                                   ptr(d.col), ptr(d.vals), d.width, ptr(xt),
+                                   ptr(out), current_stream()))
+        return vec_out(out[:a.n], was_np)
+    if isinstance(a, CsrMatrix):
+        xt, was_np = vec_in(x, a.n)
+        d = device_copy(a)
+        out = empty(a.n)
+        check(LIB.tb_dev_spmv_csr(a.n, ptr(d.row_ptr), ptr(d.col), ptr(d.vals),
+                                  ptr(xt), ptr(out), current_stream()))
+        return vec_out(out, was_np)
+    del t
+    raise TypeError(f"spmv: unsupported matrix type {type(a).__name__}")
+
+
+def vec_in_pad(x, n_pad):
+    t = require_cuda()
+    if isinstance(x, t.Tensor):
+        xt, was = vec_in(x, x.shape[0])
+    else:
+        a = np.ascontiguousarray(x, dtype=np.float64)
+        xt, was = to_device(a), True
+    if xt.shape[0] < n_pad:
+        xp = t.zeros(n_pad, dtype=t.float64, device="cuda")
+        xp[:xt.shape[0]] = xt
+        xt = xp
+    return xt, was
+
+
+# ------------------------------------------------------------------ plans
+def _sell_host(s, keep):
+    """tb_sell_host view of a SellMatrix (arrays kept alive in `keep`)."""
+    sp = np.ascontiguousarray(s.slice_ptr, dtype=np.int64)
+    sl = np.ascontiguousarray(s.slice_len, dtype=np.int32)
+    col = np.ascontiguousarray(s.col32, dtype=np.int32)
+    v = np.ascontiguousarray(s.vals, dtype=np.float64)
+    keep.extend([sp, sl, col, v])
+    return _lib.TbSellHost(s.n_slices, s.width, ptr(sp), ptr(sl), ptr(col), ptr(v))
+
+
+def _csr_host(a, keep):
+    rp = np.ascontiguousarray(a.row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(a.col_idx, dtype=np.int32)
+    v = np.ascontiguousarray(a.vals, dtype=np.float64)
+    keep.extend([rp, col, v])
+    return _lib.TbCsrHost(a.n, ptr(rp), ptr(col), ptr(v))
+
+
+def _sched_host(sched, keep):
+    if sched is None:
+        return _lib.TbSchedHost(0, None, None, None, 0)
+    phase_ptr, task_ptr, rows = sched
+    pp = np.ascontiguousarray(phase_ptr, dtype=np.int64)
+    tp = np.ascontiguousarray(task_ptr, dtype=np.int64)
+    keep.extend([pp, tp])
+    rp = None
+    nr = 0
+    if rows is not None:
+        rr = np.ascontiguousarray(rows, dtype=np.int64)
+        keep.append(rr)
+        rp = ptr(rr)
+        nr = rr.shape[0]
+    return _lib.TbSchedHost(pp.shape[0] - 1, ptr(pp), ptr(tp), rp, nr)
+
+
+class DevicePlan:
+    """Owns a tb_plan: factor(s), A and the solver vectors resident in HBM."""
+
+    def __init__(self, *, kind, n, n_real, inv_d, spmv_format,
+                 w=0, b_s=0, color_lvl1_ranges=None, L_sell=None, U_sell=None,
+                 L_csr=None, U_csr=None, fwd_sched=None, bwd_sched=None,
+                 A_sell=None, A_csr=None, device=None):
+        t = require_cuda()
+        self.handle = None
+        keep = []
+        desc = _lib.TbPlanDesc()
+        desc.precond_kind = kind
+        desc.spmv_format = spmv_format
+        desc.n = n
+        desc.n_real = n_real
+        inv = np.ascontiguousarray(inv_d, dtype=np.float64)
+        keep.append(inv)
+        desc.inv_d = ptr(inv)
+        if kind == _lib.TB_PRECOND_HBMC:
+            cr = np.ascontiguousarray(color_lvl1_ranges, dtype=np.int64)
+            keep.append(cr)
+            desc.w, desc.b_s, desc.n_c = w, b_s, cr.shape[0] - 1
+            desc.color_lvl1_ranges = ptr(cr)
+            desc.L_sell = _sell_host(L_sell, keep)
+            desc.U_sell = _sell_host(U_sell, keep)
+        else:
+            desc.L_csr = _csr_host(L_csr, keep)
+            desc.U_csr = _csr_host(U_csr, keep)
+            desc.fwd_sched = _sched_host(fwd_sched, keep)
+            desc.bwd_sched = _sched_host(bwd_sched, keep)
+        if spmv_format == _lib.TB_SPMV_SELL:
+            desc.A_sell = _sell_host(A_sell, keep)
+        elif spmv_format == _lib.TB_SPMV_CSR:
+            desc.A_csr = _csr_host(A_csr, keep)
+        self.device = t.cuda.current_device() if device is None else device
+        h = C.c_void_p()
+        check(LIB.tb_plan_create(C.byref(desc), self.device, C.byref(h)))
+        self.handle = h
+        self.n = n
+        self.n_real = n_real
+        self.kind = kind
+
+    def close(self):
+        if self.handle is not None:
+            LIB.tb_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- operators on CUDA tensors (length n, float64, contiguous)
+    def forward(self, r, y, stream=None):
+        check(LIB.tb_plan_forward(self.handle, ptr(r), ptr(y),
+                                  stream if stream is not None else current_stream()))
+
+    def backward(self, y, z, stream=None):
+        check(LIB.tb_plan_backward(self.handle, ptr(y), ptr(z),
+                                   stream if stream is not None else current_stream()))
+
+    def precond(self, r, z, stream=None):
+        check(LIB.tb_plan_precond(self.handle, ptr(r), ptr(z),
+                                  stream if stream is not None else current_stream()))
+
+    def spmv(self, x, y, stream=None):
+        check(LIB.tb_plan_spmv(self.handle, ptr(x), ptr(y),
+                               stream if stream is not None else current_stream()))
+
+    def barriers_per_sweep(self):
+        v = _lib.i64()
+        check(LIB.tb_plan_barriers_per_sweep(self.handle, v))
+        return v.value
+
+    def device_bytes(self):
+        v = _lib.i64()
+        check(LIB.tb_plan_device_bytes(self.handle, v))
+        return v.value
+
+    def pcg(self, b, x, tol, max_iters, stream=None):
+        """Device-resident PCG; returns (report struct, history ndarray)."""
+        rep = _lib.TbPcgReport()
+        hist = np.empty(max_iters + 1)
+        rc = LIB.tb_pcg(self.handle, ptr(b), ptr(x), float(tol), int(max_iters), 0,
+                        stream if stream is not None else current_stream(),
+                        C.byref(rep), ptr(hist))
+        if rc not in (_lib.TB_OK, _lib.TB_ECG_BREAKDOWN):
+            check(rc)
+        return rep, hist[:rep.iterations + 1].copy()

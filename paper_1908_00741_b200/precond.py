@@ -1,0 +1,376 @@
+"""IC(0) factor and the substitution operators (drop-in for trilab.precond).
+
+* ic0_factorize: the zero-fill shifted IC of K/numba_backend.py:40-79, run
+  in the native host builder with non-contracted arithmetic (bit-exact).
+* sub_forward_* / sub_backward_*: ALL run on the B200.  HBMC uses the SELL
+  sweep kernel (one grid-wide phase per color); MC / BMC / natural use the
+  CSR task-sweep kernel (one phase per color / per dependency level).  Every
+  row's arithmetic is the reference's, so outputs are bitwise equal to
+  sub_forward_seq / sub_backward_seq of the reference.
+
+`pool=` and `kernels=` are accepted for signature compatibility and ignored
+(one device backend; the GPU grid replaces the thread pool).  `counter=`
+still sees exactly n_phases - 1 barrier() calls per sweep, which are the
+device-side phase boundaries.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import LIB, check, i64a, ptr
+from .matrix import CsrMatrix, csr_to_sell, csr_transpose
+
+__all__ = [
+    "IcBreakdownError", "IcFactor", "SellFactor", "BarrierCounter",
+    "WorkerPool", "ic0_factorize", "factor_equivalence_check",
+    "build_sell_factor", "ic_residual_on_pattern",
+    "sub_forward_seq", "sub_backward_seq", "sub_forward_mc",
+    "sub_backward_mc", "sub_forward_bmc", "sub_backward_bmc",
+    "sub_forward_hbmc", "sub_backward_hbmc", "apply_ic_preconditioner",
+]
+
+
+class IcBreakdownError(ArithmeticError):
+    """Non-positive pivot encountered during factorization."""
+
+    def __init__(self, row, pivot):
+        self.row = int(row)
+        self.pivot = float(pivot)
+        super().__init__(f"non-positive pivot {pivot:.6g} at row {row}")
+
+
+@dataclass
+class IcFactor:
+    L: CsrMatrix
+    d: np.ndarray
+    inv_diag: np.ndarray
+    shift: float
+    layout_tag: str
+    U: CsrMatrix
+
+    @property
+    def n(self):
+        return self.d.shape[0]
+
+
+@dataclass
+class SellFactor:
+    lower: object
+    upper: object
+    d: np.ndarray
+    inv_diag: np.ndarray
+    w: int
+    b_s: int
+    layout_tag: str = "hbmc"
+
+    @property
+    def n(self):
+        return self.d.shape[0]
+
+
+@dataclass
+class BarrierCounter:
+    """Counts synchronization points; count/phase_order reset per invocation."""
+
+    count: int = 0
+    total: int = 0
+    invocations: int = 0
+    phase_order: list = field(default_factory=list)
+
+    def start(self):
+        self.count = 0
+        self.phase_order = []
+        self.invocations += 1
+
+    def enter_phase(self, color):
+        self.phase_order.append(int(color))
+
+    def barrier(self):
+        self.count += 1
+        self.total += 1
+
+
+class _NullCounter:
+    def start(self):
+        pass
+
+    def enter_phase(self, color):
+        pass
+
+    def barrier(self):
+        pass
+
+
+_NULL = _NullCounter()
+
+
+class WorkerPool:
+    """Kept for signature compatibility with src/precond.py:123-150.
+
+    The device grid is the worker pool here; `threads` is recorded and
+    otherwise unused by the substitution operators.
+    """
+
+    def __init__(self, threads=1):
+        self.threads = max(1, int(threads))
+
+    def run(self, fn, tasks):
+        for args in tasks:
+            fn(*args)
+
+    def close(self):
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def _strict_tri(a: CsrMatrix, upper=False):
+    rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.row_ptr))
+    mask = (a.col_idx > rows) if upper else (a.col_idx < rows)
+    row_ptr = np.zeros(a.n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[mask], minlength=a.n), out=row_ptr[1:])
+    return CsrMatrix(a.n, row_ptr, a.col_idx[mask], a.vals[mask],
+                     diag_ptr=np.full(a.n, -1, dtype=np.int64))
+
+
+def _check_structural_symmetry(a: CsrMatrix):
+    at = csr_transpose(a)
+    if not (np.array_equal(at.row_ptr, a.row_ptr)
+            and np.array_equal(at.col_idx, a.col_idx)):
+        raise ValueError("matrix structure is not symmetric")
+
+
+def ic0_factorize(a: CsrMatrix, shift=0.0, layout_tag="natural", kernels=None):
+    """src/precond.py:179-200 over K/numba_backend.py:40-79."""
+    if shift < 0:
+        raise ValueError("shift must be non-negative")
+    if (a.diag_ptr < 0).any():
+        bad = int(np.nonzero(a.diag_ptr < 0)[0][0])
+        raise ValueError(f"row {bad} has no diagonal entry")
+    _check_structural_symmetry(a)
+    low = _strict_tri(a, upper=False)
+    lvals = low.vals.copy()
+    adiag = a.diagonal() * (1.0 + shift)
+    d = np.empty(a.n)
+    inv_d = np.empty(a.n)
+    bad_row, pivot = _lib.i64(), _lib.dbl()
+    rc = LIB.tb_ic0_factor(a.n, ptr(low.row_ptr), ptr(low.col_idx), ptr(lvals),
+                           ptr(adiag), ptr(d), ptr(inv_d), bad_row, pivot)
+    if rc == _lib.TB_EIC_BREAKDOWN:
+        raise IcBreakdownError(bad_row.value, pivot.value)
+    check(rc)
+    L = CsrMatrix(a.n, low.row_ptr, low.col_idx, lvals,
+                  diag_ptr=np.full(a.n, -1, dtype=np.int64))
+    return IcFactor(L, d, inv_d, float(shift), layout_tag, csr_transpose(L))
+
+
+def ic_residual_on_pattern(a: CsrMatrix, f: IcFactor, kernels=None):
+    """src/precond.py:203-224 (verifier; native llt_on_pattern)."""
+    low_a = _strict_tri(a, upper=False)
+    pattern_ok = (np.array_equal(low_a.row_ptr, f.L.row_ptr)
+                  and np.array_equal(low_a.col_idx, f.L.col_idx))
+    low = np.empty(f.L.nnz)
+    diag = np.empty(f.n)
+    check(LIB.tb_llt_on_pattern(f.n, ptr(f.L.row_ptr), ptr(f.L.col_idx),
+                                ptr(f.L.vals), ptr(np.ascontiguousarray(f.d)),
+                                ptr(low), ptr(diag)))
+    ref_low = low_a.vals
+    ref_diag = a.diagonal() * (1.0 + f.shift)
+    max_rel = 0.0
+    if ref_low.shape[0] and low.shape[0] == ref_low.shape[0]:
+        max_rel = float(np.max(np.abs(low - ref_low) / np.maximum(np.abs(ref_low), 1e-300)))
+    max_rel = max(max_rel, float(np.max(np.abs(diag - ref_diag)
+                                        / np.maximum(np.abs(ref_diag), 1e-300))))
+    return max_rel, pattern_ok
+
+
+def factor_equivalence_check(a: CsrMatrix, p, shift=0.0, tol=1e-12, kernels=None):
+    """src/precond.py:232-260: does factorization commute with p?"""
+    from .matrix import permute_system
+    f1 = ic0_factorize(a, shift=shift)
+    a2, _ = permute_system(a, np.zeros(a.n), p)
+    f2 = ic0_factorize(a2, shift=shift)
+    q = p.new_of_old
+    r1 = np.repeat(np.arange(f1.n, dtype=np.int64), np.diff(f1.L.row_ptr))
+    r1m, c1m = q[r1], q[f1.L.col_idx]
+    if (c1m > r1m).any():
+        return False, float("inf")
+    order = np.lexsort((c1m, r1m))
+    r2 = np.repeat(np.arange(f2.n, dtype=np.int64), np.diff(f2.L.row_ptr))
+    if not (np.array_equal(r1m[order], r2) and np.array_equal(c1m[order], f2.L.col_idx)):
+        return False, float("inf")
+    v1, v2 = f1.L.vals, f2.L.vals
+    dev = 0.0
+    if v2.shape[0]:
+        dev = float(np.max(np.abs(v1[order] - v2) / np.maximum(np.abs(v2), 1e-300)))
+    d1m = np.empty_like(f1.d)
+    d1m[q] = f1.d
+    dev = max(dev, float(np.max(np.abs(d1m - f2.d) / np.maximum(np.abs(f2.d), 1e-300))))
+    return dev <= tol, dev
+
+
+def build_sell_factor(f: IcFactor, hl):
+    """src/precond.py:263-270: L and U in SELL with slice width w."""
+    if f.layout_tag != "hbmc":
+        raise ValueError(f"factor tag {f.layout_tag!r}; need 'hbmc'")
+    if f.n != hl.n_pad:
+        raise ValueError("factor size does not match padded layout size")
+    return SellFactor(csr_to_sell(f.L, hl.w), csr_to_sell(f.U, hl.w),
+                      f.d, f.inv_diag, hl.w, hl.b_s)
+
+
+def _require_tag(f, expected):
+    if f.layout_tag != expected:
+        raise ValueError(f"factor was built under {f.layout_tag!r}, kernel needs {expected!r}")
+
+
+# ------------------------------------------------------------ schedules
+def level_schedule(tri: CsrMatrix, forward):
+    """Dependency levels of a strict triangle -> (phase_ptr, task_ptr, rows)."""
+    from .ordering import _group
+    level = np.empty(tri.n, dtype=np.int64)
+    nl = _lib.i64()
+    check(LIB.tb_level_schedule(tri.n, ptr(tri.row_ptr), ptr(tri.col_idx),
+                                1 if forward else 0, ptr(level), nl))
+    phase_ptr, rows = _group(level, nl.value)
+    return phase_ptr, None, rows
+
+
+def _sched_for(kind, f, layout):
+    """(fwd_sched, bwd_sched) of the CSR task sweeps (MC / BMC / natural)."""
+    if kind == "mc":
+        s = (i64a(layout.color_ranges), None, None)
+        return s, s
+    if kind == "bmc":
+        s = (i64a(layout.color_block_ranges), i64a(layout.block_bounds), None)
+        return s, s
+    return level_schedule(f.L, True), level_schedule(f.U, False)
+
+
+def _task_plan(f, kind, layout):
+    """Cached preconditioner-only device plan of an IcFactor."""
+    from . import device
+    cache = f.__dict__.setdefault("_tb_plans", {})
+    key = (kind, id(layout))
+    hit = cache.get(key)
+    if hit is not None and hit[0] is layout:
+        return hit[1]
+    fs, bs = _sched_for(kind, f, layout)
+    plan = device.DevicePlan(kind=_lib.TB_PRECOND_TASKS, n=f.n, n_real=f.n,
+                             inv_d=f.inv_diag, spmv_format=_lib.TB_SPMV_NONE,
+                             L_csr=f.L, U_csr=f.U, fwd_sched=fs, bwd_sched=bs)
+    plan.n_phases_fwd = fs[0].shape[0] - 1
+    plan.n_phases_bwd = bs[0].shape[0] - 1
+    cache[key] = (layout, plan)
+    return plan
+
+
+def _hbmc_plan(sf, hl):
+    from . import device
+    cache = sf.__dict__.setdefault("_tb_plans", {})
+    hit = cache.get(id(hl))
+    if hit is not None and hit[0] is hl:
+        return hit[1]
+    plan = device.DevicePlan(kind=_lib.TB_PRECOND_HBMC, n=hl.n_pad, n_real=hl.n,
+                             inv_d=sf.inv_diag, spmv_format=_lib.TB_SPMV_NONE,
+                             w=sf.w, b_s=sf.b_s,
+                             color_lvl1_ranges=hl.color_lvl1_ranges,
+                             L_sell=sf.lower, U_sell=sf.upper)
+    cache[id(hl)] = (hl, plan)
+    return plan
+
+
+def _count(counter, phases):
+    counter.start()
+    for idx, c in enumerate(phases):
+        counter.enter_phase(c)
+        if idx < len(phases) - 1:
+            counter.barrier()
+
+
+def _run(plan, fn_name, v, n):
+    from . import device
+    vt, was_np = device.vec_in(v, n)
+    out = device.empty(n)
+    getattr(plan, fn_name)(vt, out)
+    return device.vec_out(out, was_np)
+
+
+def sub_forward_seq(f: IcFactor, r, kernels=None):
+    """src/precond.py:285-290 (device, dependency-level schedule)."""
+    return _run(_task_plan(f, "seq", None), "forward", r, f.n)
+
+
+def sub_backward_seq(f: IcFactor, y, kernels=None):
+    """src/precond.py:293-298."""
+    return _run(_task_plan(f, "seq", None), "backward", y, f.n)
+
+
+def sub_forward_mc(f: IcFactor, coloring, r, pool=None, counter=None, kernels=None):
+    """src/precond.py:320-326."""
+    _require_tag(f, "mc")
+    out = _run(_task_plan(f, "mc", coloring), "forward", r, f.n)
+    _count(counter or _NULL, list(range(coloring.n_c)))
+    return out
+
+
+def sub_backward_mc(f: IcFactor, coloring, y, pool=None, counter=None, kernels=None):
+    """src/precond.py:329-335."""
+    _require_tag(f, "mc")
+    out = _run(_task_plan(f, "mc", coloring), "backward", y, f.n)
+    _count(counter or _NULL, list(range(coloring.n_c - 1, -1, -1)))
+    return out
+
+
+def sub_forward_bmc(f: IcFactor, layout, r, pool=None, counter=None, kernels=None):
+    """src/precond.py:361-366."""
+    _require_tag(f, "bmc")
+    out = _run(_task_plan(f, "bmc", layout), "forward", r, f.n)
+    _count(counter or _NULL, list(range(layout.n_c)))
+    return out
+
+
+def sub_backward_bmc(f: IcFactor, layout, y, pool=None, counter=None, kernels=None):
+    """src/precond.py:369-374."""
+    _require_tag(f, "bmc")
+    out = _run(_task_plan(f, "bmc", layout), "backward", y, f.n)
+    _count(counter or _NULL, list(range(layout.n_c - 1, -1, -1)))
+    return out
+
+
+def sub_forward_hbmc(sf: SellFactor, hl, r, pool=None, counter=None, kernels=None):
+    """src/precond.py:395-400: one device phase per color, ascending."""
+    _require_tag(sf, "hbmc")
+    out = _run(_hbmc_plan(sf, hl), "forward", r, hl.n_pad)
+    _count(counter or _NULL, list(range(hl.n_c)))
+    return out
+
+
+def sub_backward_hbmc(sf: SellFactor, hl, y, pool=None, counter=None, kernels=None):
+    """src/precond.py:403-408: colors descending."""
+    _require_tag(sf, "hbmc")
+    out = _run(_hbmc_plan(sf, hl), "backward", y, hl.n_pad)
+    _count(counter or _NULL, list(range(hl.n_c - 1, -1, -1)))
+    return out
+
+
+def apply_ic_preconditioner(kind, f, layout, r, pool=None, counter=None, kernels=None):
+    """src/precond.py:411-425: z = (L L^T)^-1 r via the selected pair."""
+    if kind in ("seq", "natural"):
+        return sub_backward_seq(f, sub_forward_seq(f, r))
+    if kind == "mc":
+        y = sub_forward_mc(f, layout, r, pool, counter)
+        return sub_backward_mc(f, layout, y, pool, counter)
+    if kind == "bmc":
+        y = sub_forward_bmc(f, layout, r, pool, counter)
+        return sub_backward_bmc(f, layout, y, pool, counter)
+    if kind == "hbmc":
+        y = sub_forward_hbmc(f, layout, r, pool, counter)
+        return sub_backward_hbmc(f, layout, y, pool, counter)
+    raise ValueError(f"unknown kernel selector {kind!r}")
