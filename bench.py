@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark: HBMC IC(0) fwd+bwd substitution GB/s and ICCG time-to-solution.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2]
+
+Workload (BASELINE.json configs[1]): 3-D variable-coefficient 7-point
+diffusion on 128^3, HBMC b_s=8, w=32, fp64, synthetic seeded inputs
+(SURVEY.md Appendix B).  One "step" = one preconditioner application
+z = (L L^T)^-1 r on the device (forward + backward HBMC sweep), inputs
+resident in HBM, L2 flushed (256 MiB write) before every step.
+
+value    = algorithmic bytes of the two sweeps (2 * (12 nnz_L + 32 N), SURVEY
+           8(d)) x steps x ranks / max-over-ranks device time.
+e2e      = the same through the public API with host buffers: pinned host r
+           -> device, fwd+bwd, z -> pinned host, copies inside the timed region.
+roofline = the sweep kernel (sell_sweep, one launch per color): algorithmic
+           bytes per launch / CUDA-event launch duration vs MEASURED_PEAKS.json.
+iccg     = full PCG solve to 1e-7 on the device (one CUDA-graph launch).
+cpu_baseline = the CPU oracle port of the reference path (oracle/), all host
+           threads, bounded sample of the same sweep workload (rank 0, N=1).
+
+N > 1: every rank solves its own replica of the problem (no data-path
+collective); timing is the max over ranks (scaling "weak").
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "HBMC IC(0) fwd+bwd substitution GB/s (algorithmic bytes)"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def sweep_bytes(nnz_l, n):
+    """S = 12 nnz_L + 32 N per sweep (int32 idx, fp64 values)."""
+    return 12 * nnz_l + 32 * n
+
+
+def spmv_bytes(nnz_a, n):
+    return 12 * nnz_a + 16 * n
+
+
+def load_peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.QUERY,
+                     "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_problem(cfg_id):
+    from paper_1908_00741_b200 import problems
+    label, gen, bs, w = problems.CONFIGS[cfg_id]
+    t0 = time.perf_counter()
+    a = gen()
+    xs, b = problems.rhs(a)
+    return label, a, xs, b, bs, w, time.perf_counter() - t0
+
+
+def cpu_baseline(a, b, bs, w, steps, warmup, threads):
+    """Oracle port of the reference CPU path: fwd+bwd HBMC sweep, GB/s."""
+    from oracle import oracle as O
+    oa = O.Csr(a.n, a.row_ptr, a.col_idx, a.vals)
+    osys = O.HbmcSystem(oa, b, bs, w)
+    r = np.random.default_rng(0).standard_normal(osys.hl["n_pad"])
+    for _ in range(warmup):
+        osys.precond(r, threads)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        osys.precond(r, threads)
+        ts.append(time.perf_counter() - t0)
+    nbytes = 2 * sweep_bytes(osys.nnz_L, a.n)
+    return {"value": nbytes * len(ts) / sum(ts) / 1e9, "unit": "GB/s",
+            "cores": threads, "kind": "port",
+            "sample": f"{len(ts)} fwd+bwd HBMC sweeps of the full workload "
+                      f"(oracle/hbmc_oracle.c, per-color fork-join over {threads} "
+                      f"OpenMP threads as src/precond.py:377-392)",
+            "ms_per_step": 1e3 * sum(ts) / len(ts),
+            "setup_s": osys.time_setup_s}, osys
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    label, a, xs, b, bs, w, _ = build_problem(args.config)
+    threads = O.max_threads()
+    cb, osys = cpu_baseline(a, b, bs, w, args.steps, args.warmup, threads)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, SURVEY Appendix B)",
+            "config": {"workload": f"config{args.config} {label} b_s={bs} w={w}",
+                       "N": a.n, "nnz_L": osys.nnz_L},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1908_00741_b200 as P
+    from paper_1908_00741_b200 import _lib, solver
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    label, a, xs, b, bs, w, t_gen = build_problem(args.config)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    t0 = time.perf_counter()
+    setup = solver.prepare(a, b, cfg)
+    solver.attach_plan(setup, cfg)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    plan, hl, sf = setup.plan, setup.layout, setup.factor
+    n_pad = hl.n_pad
+    nnz_l = int((a.nnz - a.n) // 2)   # strictly-lower nonzeros of A (= of L)
+    S = sweep_bytes(nnz_l, a.n)
+    step_bytes = 2 * S
+
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    r = torch.from_numpy(np.random.default_rng(0).standard_normal(n_pad)).to(dev)
+    z = torch.empty_like(r)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- device-resident steps (value)
+    for _ in range(args.warmup):
+        flush.zero_()
+        plan.precond(r, z, sptr)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record(stream)
+            plan.precond(r, z, sptr)
+            e1.record(stream)
+        barrier()
+    dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+    launches = 2 * hl.n_c * args.steps
+
+    # ---------------- per-launch timing of the sweep kernel (roofline)
+    from paper_1908_00741_b200 import device as D
+    Ld = D.DeviceSell(sf.lower)
+    Ud = D.DeviceSell(sf.upper)
+    inv = torch.from_numpy(sf.inv_diag).to(dev)
+    y = torch.empty_like(r)
+    lv = setup.a_sys  # per-color algorithmic bytes: rows of the color + their L entries
+    rows_per_lvl1 = bs * w
+    lower_counts = np.diff(P.precond._strict_tri(lv).row_ptr)
+    upper_counts = np.diff(P.precond._strict_tri(lv, upper=True).row_ptr)
+    real = np.zeros(n_pad, dtype=bool)
+    real[hl.real_positions] = True
+    per_launch = []   # (bytes, ms)
+    for rep in range(args.warmup + args.steps):
+        flush.zero_()
+        for direction in (True, False):
+            order = range(hl.n_c) if direction else range(hl.n_c - 1, -1, -1)
+            M = Ld if direction else Ud
+            for c in order:
+                k0, k1 = int(hl.color_lvl1_ranges[c]), int(hl.color_lvl1_ranges[c + 1])
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                fn = _lib.LIB.tb_dev_fwd_sell_range if direction else _lib.LIB.tb_dev_bwd_sell_range
+                e0.record(stream)
+                _lib.check(fn(_lib.ptr(M.slice_ptr), _lib.ptr(M.slice_len), _lib.ptr(M.col),
+                              _lib.ptr(M.vals), _lib.ptr(inv), _lib.ptr(r if direction else y),
+                              _lib.ptr(y if direction else z), w, bs, k0, k1, sptr))
+                e1.record(stream)
+                if rep >= args.warmup:
+                    lo, hi = k0 * rows_per_lvl1, k1 * rows_per_lvl1
+                    cnt = (lower_counts if direction else upper_counts)[lo:hi]
+                    nb = 12 * int(cnt.sum()) + 32 * int(real[lo:hi].sum())
+                    per_launch.append((nb, e0, e1))
+    torch.cuda.synchronize()
+    tot_b = sum(p[0] for p in per_launch)
+    tot_ms = sum(p[1].elapsed_time(p[2]) for p in per_launch)
+    peak, peak_src = load_peaks()
+    achieved = tot_b / (tot_ms / 1e3) / 1e9
+
+    # ---------------- e2e through the public API (host buffers)
+    r_host = torch.from_numpy(np.random.default_rng(0).standard_normal(n_pad)).pin_memory()
+    z_host = torch.empty(n_pad, dtype=torch.float64).pin_memory()
+    r_dev = torch.empty(n_pad, dtype=torch.float64, device=dev)
+    z_dev = torch.empty_like(r_dev)
+    for _ in range(args.warmup):
+        r_dev.copy_(r_host, non_blocking=True)
+        plan.precond(r_dev, z_dev, sptr)
+        z_host.copy_(z_dev, non_blocking=True)
+    barrier()
+    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for e0, e1 in ee:
+        flush.zero_()
+        e0.record(stream)
+        r_dev.copy_(r_host, non_blocking=True)
+        plan.precond(r_dev, z_dev, sptr)
+        z_host.copy_(z_dev, non_blocking=True)
+        e1.record(stream)
+    barrier()
+    e2e_ms = sum(e0.elapsed_time(e1) for e0, e1 in ee)
+
+    # ---------------- ICCG time-to-solution on the device
+    b_dev = torch.from_numpy(setup.b_sys).to(dev)
+    x_dev = torch.empty_like(b_dev)
+    rep0, _ = plan.pcg(b_dev, x_dev, cfg.tol, cfg.max_iters)   # warm-up (graph build)
+    solves = []
+    for _ in range(3):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep, hist = plan.pcg(b_dev, x_dev, cfg.tol, cfg.max_iters, sptr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        solves.append(e0.elapsed_time(e1))
+    x_sys = x_dev.cpu().numpy()
+    x = x_sys[setup.old_positions]
+    err = float(np.linalg.norm(x - xs) / np.linalg.norm(xs))
+    # e2e solve through the public API: b on host -> x on host
+    t_e2e_solve = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xh, rep_h, _ = solver.solve_on_device(setup, cfg)
+        t_e2e_solve.append(time.perf_counter() - t0)
+
+    # ---------------- max over ranks
+    def mx(v):
+        if world == 1:
+            return v
+        tt = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    dev_ms_max = mx(dev_ms)
+    e2e_ms_max = mx(e2e_ms)
+    value = step_bytes * args.steps * world / (dev_ms_max / 1e3) / 1e9
+    e2e_val = step_bytes * args.steps * world / (e2e_ms_max / 1e3) / 1e9
+
+    line = None
+    if rank == 0:
+        cb = None
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import oracle as O
+            cb, _ = cpu_baseline(a, b, bs, w, min(args.steps, 10), 2, O.max_threads())
+        digest = os.path.join(HERE, "tests", "golden", f"config{args.config}_digest.json")
+        ref_iters = None
+        if os.path.exists(digest):
+            with open(digest) as fh:
+                ref_iters = json.load(fh)["hbmc"]["iterations"]
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, SURVEY Appendix B)",
+            "config": {"workload": f"config{args.config} {label} b_s={bs} w={w}",
+                       "N": a.n, "n_pad": n_pad, "nnz_A": int(a.nnz), "nnz_L": nnz_l,
+                       "n_c": hl.n_c, "bytes_per_step": step_bytes,
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "kernel": "sell_sweep (fwd+bwd, per color launch)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "launches": len(per_launch),
+                         "avg_launch_us": 1e3 * tot_ms / max(1, len(per_launch)),
+                         "algorithmic_bytes_per_launch": tot_b / max(1, len(per_launch)),
+                         "traffic": None},
+            "cpu_baseline": cb,
+            "e2e": {"value": e2e_val, "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * n_pad, "d2h_bytes_per_step": 8 * n_pad,
+                    "ms_per_step": e2e_ms_max / args.steps},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "iccg": {"iterations": int(rep.iterations), "reference_iterations": ref_iters,
+                     "converged": bool(rep.converged),
+                     "time_to_solution_ms": min(solves),
+                     "ms_per_iteration": min(solves) / max(1, rep.iterations),
+                     "kernel_launches": int(rep.kernel_launches),
+                     "host_syncs": int(rep.host_syncs),
+                     "rel_err_vs_xstar": err,
+                     "e2e_solve_ms": 1e3 * min(t_e2e_solve),
+                     "setup_s": t_setup, "generate_s": t_gen},
+            "spmv_bytes_per_call": spmv_bytes(int(a.nnz), a.n),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -186,8 +186,12 @@ def _sched_host(sched, keep):
         return _lib.TbSchedHost(0, None, None, None, 0)
     phase_ptr, task_ptr, rows = sched
     pp = np.ascontiguousarray(phase_ptr, dtype=np.int64)
-    tp = np.ascontiguousarray(task_ptr, dtype=np.int64)
-    keep.extend([pp, tp])
+    keep.append(pp)
+    tp_ptr = None
+    if task_ptr is not None:   # None = one row per task
+        tp = np.ascontiguousarray(task_ptr, dtype=np.int64)
+        keep.append(tp)
+        tp_ptr = ptr(tp)
     rp = None
     nr = 0
     if rows is not None:
@@ -195,7 +199,7 @@ def _sched_host(sched, keep):
         keep.append(rr)
         rp = ptr(rr)
         nr = rr.shape[0]
-    return _lib.TbSchedHost(pp.shape[0] - 1, ptr(pp), ptr(tp), rp, nr)
+    return _lib.TbSchedHost(pp.shape[0] - 1, ptr(pp), tp_ptr, rp, nr)
 
 
 class DevicePlan:

@@ -1,0 +1,9 @@
+set -x
+nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv
+nproc; free -g | head -2; lscpu | grep "Model name"
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -30 gpurun_out/pytest_gpu.log
+cat gpurun_out/smoke.log
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench_rc=$?
+tail -5 gpurun_out/bench.log

@@ -1,0 +1,133 @@
+"""Device parity against the reference's golden outputs (B200 only).
+
+Every golden case (tests/golden/*.npz, produced by the reference `trilab`
+itself, see make_golden.py) is rebuilt with this package's host builder and
+run through the CUDA kernels:
+
+* substitutions (HBMC SELL sweeps; MC / BMC / natural CSR task sweeps):
+  bitwise equal to the reference (same per-row non-FMA arithmetic);
+* SpMV (SELL and CSR): bitwise equal;
+* PCG: iteration count within +-1 of the reference (north-star bar),
+  solution within 1e-10 relative (2-norm), residual history within 1e-6
+  relative over the common prefix (dot products are reduced in a different
+  order than numpy's BLAS ddot, so the history is not bitwise).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_matrix, golden_names, load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+
+NAMES = golden_names()
+X_TOL = 1e-10          # north star: solutions agree within 1e-10 relative
+HIST_TOL = 1e-6        # residual-history agreement (not part of the bar)
+
+
+def sha(x):
+    return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+
+
+def same(g, key, arr):
+    if key in g:
+        return np.array_equal(arr, g[key])
+    return sha(arr) == str(g[key + "_sha"])
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1908_00741_b200 as P
+    return P
+
+
+def hbmc_objects(P, name):
+    a, bs, w, _ = golden_matrix(name)
+    lay = P.color_blocks(a, P.build_blocks(a, bs))
+    hl = P.build_hbmc(lay, w)
+    a_ext, b_ext = P.extend_with_dummies(a, np.zeros(a.n), hl)
+    af, _ = P.permute_system(a_ext, b_ext, hl.composed_perm)
+    f = P.ic0_factorize(af, layout_tag="hbmc")
+    sf = P.build_sell_factor(f, hl)
+    return a, lay, hl, af, f, sf
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_hbmc_sweeps_bitwise(P, name):
+    g = load_golden(name)
+    a, lay, hl, af, f, sf = hbmc_objects(P, name)
+    assert np.array_equal(hl.composed_perm.new_of_old, g["composed"])
+    r = np.random.default_rng(0).standard_normal(hl.n_pad)
+    bc = P.BarrierCounter()
+    y = P.sub_forward_hbmc(sf, hl, r, counter=bc)
+    assert bc.count == hl.n_c - 1
+    z = P.sub_backward_hbmc(sf, hl, y, counter=bc)
+    assert bc.phase_order == list(range(hl.n_c))[::-1]
+    assert same(g, "y", y), "forward sweep differs from the reference"
+    assert same(g, "z", z), "backward sweep differs from the reference"
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_spmv_bitwise(P, name):
+    g = load_golden(name)
+    a, lay, hl, af, f, sf = hbmc_objects(P, name)
+    x = np.random.default_rng(2).standard_normal(hl.n_pad)
+    ys = P.spmv(P.csr_to_sell(af, hl.w), x)
+    yc = P.spmv(af, x)
+    assert same(g, "spmv_sell", ys)
+    assert same(g, "spmv_csr", yc)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_csr_task_sweeps_bitwise(P, name):
+    g = load_golden(name)
+    a, bs, w, _ = golden_matrix(name)
+    r = np.random.default_rng(0).standard_normal(int(g["n_pad"]))[:a.n]
+    nod = P.greedy_color_nodes(a)
+    ap, _ = P.permute_system(a, np.zeros(a.n), nod.perm)
+    fm = P.ic0_factorize(ap, layout_tag="mc")
+    ym = P.sub_forward_mc(fm, nod, r)
+    assert same(g, "mc_y", ym)
+    assert same(g, "mc_z", P.sub_backward_mc(fm, nod, ym))
+    lay = P.color_blocks(a, P.build_blocks(a, bs))
+    ab, _ = P.permute_system(a, np.zeros(a.n), lay.perm)
+    fb = P.ic0_factorize(ab, layout_tag="bmc")
+    yb = P.sub_forward_bmc(fb, lay, r)
+    assert same(g, "bmc_y", yb)
+    assert same(g, "bmc_z", P.sub_backward_bmc(fb, lay, yb))
+    fn = P.ic0_factorize(a)
+    yn = P.sub_forward_seq(fn, r)
+    assert same(g, "nat_y", yn)
+    assert same(g, "nat_z", P.sub_backward_seq(fn, yn))
+
+
+@pytest.mark.parametrize("ordering", ["hbmc", "bmc", "mc", "natural"])
+@pytest.mark.parametrize("name", NAMES)
+def test_pcg_matches_reference(P, name, ordering):
+    g = load_golden(name)
+    a, bs, w, rhs_kind = golden_matrix(name)
+    if rhs_kind == "ones":
+        b = np.ones(a.n)
+    else:
+        from paper_1908_00741_b200 import problems
+        _, b = problems.rhs(a)
+    cfg = P.CgConfig(ordering=ordering, b_s=bs, w=w,
+                     spmv_format="sell" if ordering == "hbmc" else "crs")
+    x, rep = P.pcg(a, b, cfg)
+    it_ref = int(g[f"pcg_{ordering}_iters"])
+    assert rep.converged == bool(g[f"pcg_{ordering}_converged"])
+    assert abs(rep.iterations - it_ref) <= 1, (rep.iterations, it_ref)
+    assert rep.barrier_total == int(g[f"pcg_{ordering}_barriers"])
+    h = np.asarray(rep.residual_history)
+    href = g[f"pcg_{ordering}_hist"]
+    m = min(h.shape[0], href.shape[0])
+    assert h[0] == href[0]
+    assert np.max(np.abs(h[:m] - href[:m]) / np.maximum(href[:m], 1e-300)) <= HIST_TOL
+    key = f"pcg_{ordering}_x"
+    if key in g:
+        assert rel_err(x, g[key]) <= X_TOL
