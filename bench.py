@@ -213,33 +213,29 @@ def run_ours(args, rank, world, local_rank):
     launches = 2 * hl.n_c * args.steps
 
     # ---------------- per-launch timing of the sweep kernel (roofline)
-    from paper_1908_00741_b200 import device as D
-    Ld = D.DeviceSell(sf.lower)
-    Ud = D.DeviceSell(sf.upper)
-    inv = torch.from_numpy(sf.inv_diag).to(dev)
     y = torch.empty_like(r)
-    lv = setup.a_sys  # per-color algorithmic bytes: rows of the color + their L entries
     rows_per_lvl1 = bs * w
-    lower_counts = np.diff(P.precond._strict_tri(lv).row_ptr)
-    upper_counts = np.diff(P.precond._strict_tri(lv, upper=True).row_ptr)
+    lower_counts = np.diff(P.precond._strict_tri(setup.a_sys).row_ptr)
+    upper_counts = np.diff(P.precond._strict_tri(setup.a_sys, upper=True).row_ptr)
     real = np.zeros(n_pad, dtype=bool)
     real[hl.real_positions] = True
-    per_launch = []   # (bytes, ms)
-    for rep in range(args.warmup + args.steps):
+    kernel_info = [dict(plan.phase_info(fw, c), forward=fw, color=c)
+                   for fw in (True, False) for c in range(hl.n_c)]
+    per_launch = []   # (algorithmic bytes, start event, end event)
+    for rep_i in range(args.warmup + args.steps):
         flush.zero_()
         for direction in (True, False):
             order = range(hl.n_c) if direction else range(hl.n_c - 1, -1, -1)
-            M = Ld if direction else Ud
             for c in order:
                 k0, k1 = int(hl.color_lvl1_ranges[c]), int(hl.color_lvl1_ranges[c + 1])
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                fn = _lib.LIB.tb_dev_fwd_sell_range if direction else _lib.LIB.tb_dev_bwd_sell_range
                 e0.record(stream)
-                _lib.check(fn(_lib.ptr(M.slice_ptr), _lib.ptr(M.slice_len), _lib.ptr(M.col),
-                              _lib.ptr(M.vals), _lib.ptr(inv), _lib.ptr(r if direction else y),
-                              _lib.ptr(y if direction else z), w, bs, k0, k1, sptr))
+                if direction:
+                    plan.sweep_phase(True, c, r, y, sptr)
+                else:
+                    plan.sweep_phase(False, c, y, z, sptr)
                 e1.record(stream)
-                if rep >= args.warmup:
+                if rep_i >= args.warmup:
                     lo, hi = k0 * rows_per_lvl1, k1 * rows_per_lvl1
                     cnt = (lower_counts if direction else upper_counts)[lo:hi]
                     nb = 12 * int(cnt.sum()) + 32 * int(real[lo:hi].sum())
@@ -337,7 +333,7 @@ def run_ours(args, rank, world, local_rank):
                          "launches": len(per_launch),
                          "avg_launch_us": 1e3 * tot_ms / max(1, len(per_launch)),
                          "algorithmic_bytes_per_launch": tot_b / max(1, len(per_launch)),
-                         "traffic": None},
+                         "traffic": None, "phases": kernel_info},
             "cpu_baseline": cb,
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_pad, "d2h_bytes_per_step": 8 * n_pad,

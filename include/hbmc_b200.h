@@ -251,6 +251,14 @@ int tb_plan_backward(tb_plan *plan, const double *y, double *z, void *stream);
 int tb_plan_precond(tb_plan *plan, const double *r, double *z, void *stream);
 /* src/matrix.py:307-323 spmv with the plan's A. */
 int tb_plan_spmv(tb_plan *plan, const double *x, double *y, void *stream);
+/* One color phase of the HBMC forward (forward=1, L) or backward (U) sweep:
+ * the unit the plan launches between two grid-wide phase boundaries. */
+int tb_plan_sweep_phase(tb_plan *plan, int forward, int64_t phase,
+                        const double *src, double *dst, void *stream);
+/* Which sweep kernel a phase uses: staged (TMA) or simple, and its launch. */
+int tb_plan_phase_info(const tb_plan *plan, int forward, int64_t phase,
+                       int32_t *staged, int32_t *warps, int32_t *grid,
+                       int32_t *max_slots);
 /* number of grid-wide phase boundaries one sweep crosses (n_c - 1) */
 int tb_plan_barriers_per_sweep(const tb_plan *plan, int64_t *count);
 

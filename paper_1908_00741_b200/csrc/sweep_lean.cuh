@@ -1,0 +1,133 @@
+// HBMC substitution sweep, lean thread-per-lane version (sm_100a).
+//
+// Same arithmetic as K/numba_backend.py:132-171, bitwise.  One thread per
+// (level-1 block k, lane j); the thread walks its b_s rows.  The walk is a
+// chain of dependent steps, so the kernel is built to keep DRAM traffic in
+// flight while each step waits on its gathers, with a short instruction
+// stream:
+//   * all step descriptors (slice offset, length) are loaded up front into
+//     the thread's column of shared memory;
+//   * the first KC slots (columns + values), rhs and inv_d of step i+1 are
+//     loaded while step i issues its gathers and runs its chain -- two
+//     register buffers used ping-pong (the step loop is unrolled by two), so
+//     no register copies; slots beyond KC (rare) are loaded synchronously;
+//   * with W = 32 known at compile time every slot load is an immediate
+//     offset from one base pointer per step;
+//   * in-block operands (same lane, earlier step) are read back from the
+//     thread's results in shared memory;
+//   * 32-bit row / column / slot arithmetic (the host checks the ranges).
+// Products __dmul_rn, updates __dsub_rn, slot order = the reference's; a
+// padding slot (col == own row, v == 0) multiplies the in-progress value.
+
+#pragma once
+
+namespace sweep_lean {
+
+template <int KC>
+struct Buf {
+  int c[KC];
+  double v[KC];
+  double rhs, idg;
+};
+
+// W > 0: compile-time slice width; W == 0: runtime w
+template <bool FWD, int KC, int W>
+__global__ void __launch_bounds__(256)
+    sweep_kernel(const long long *__restrict__ slice_ptr, const int *__restrict__ slice_len,
+                 const int *__restrict__ col, const double *__restrict__ val,
+                 const double *__restrict__ inv_d, const double *__restrict__ src,
+                 double *__restrict__ dst, int w_rt, int b_s, int k0, int nthreads,
+                 const int *done) {
+  // shared: ys[b_s][T] doubles | offs[b_s][T] ints | lens[b_s][T] ints
+  extern __shared__ __align__(16) double ys[];
+  if (done && *(const volatile int *)done) return;
+  const int w = W > 0 ? W : w_rt;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nthreads) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  int *offs = (int *)(ys + (size_t)b_s * nt);
+  int *lens = offs + (size_t)b_s * nt;
+  const int kq = g / w;
+  const int j = g - kq * w;
+  const int k = k0 + kq;
+  const int span = b_s * w;
+  const int blk0 = k * span;
+  const unsigned uspan = (unsigned)span;
+
+  // walk step i is slice sid(i) = k*b_s + (FWD ? i : b_s-1-i)
+  for (int i = 0; i < b_s; ++i) {
+    const int sid = k * b_s + (FWD ? i : b_s - 1 - i);
+    offs[i * nt + tid] = (int)slice_ptr[sid] + j;
+    lens[i * nt + tid] = slice_len[sid];
+  }
+
+  auto load = [&](int i, Buf<KC> &b) {
+    const int off = offs[i * nt + tid], len = lens[i * nt + tid];
+    const int row = blk0 + (FWD ? i : b_s - 1 - i) * w + j;
+    const int *cp = col + off;
+    const double *vp = val + off;
+#pragma unroll
+    for (int u = 0; u < KC; ++u) {
+      const bool in = u < len;
+      b.c[u] = in ? __ldg(cp + u * w) : row;
+      b.v[u] = in ? __ldg(vp + u * w) : 0.0;
+    }
+    b.rhs = __ldg(src + row);
+    b.idg = __ldg(inv_d + row);
+  };
+
+  auto step = [&](int i, const Buf<KC> &b) {
+    const int l = FWD ? i : b_s - 1 - i;
+    const int row = blk0 + l * w + j;
+    const int len = lens[i * nt + tid];
+    double x[KC];
+#pragma unroll
+    for (int u = 0; u < KC; ++u) {
+      const bool inblk = (unsigned)(b.c[u] - blk0) < uspan;
+      x[u] = inblk ? 0.0 : __ldg(dst + b.c[u]);
+    }
+    double y = b.rhs;
+    auto update = [&](int cc, double vv, double xcross) {
+      double xv = xcross;
+      if ((unsigned)(cc - blk0) < uspan) {
+        if (cc == row) {
+          xv = y;
+        } else {
+          const int lp = (cc - blk0) / w;
+          xv = ys[(FWD ? lp : b_s - 1 - lp) * nt + tid];
+        }
+      }
+      y = __dsub_rn(y, __dmul_rn(vv, xv));
+    };
+#pragma unroll
+    for (int u = 0; u < KC; ++u)
+      if (u < len) update(b.c[u], b.v[u], x[u]);
+    if (len > KC) {  // long row: remaining slots synchronously
+      const int off = offs[i * nt + tid];
+      for (int t = KC; t < len; ++t) {
+        const int cc = __ldg(col + off + t * w);
+        const double vv = __ldg(val + off + t * w);
+        const double xc = (unsigned)(cc - blk0) < uspan ? 0.0 : __ldg(dst + cc);
+        update(cc, vv, xc);
+      }
+    }
+    y = __dmul_rn(y, b.idg);
+    ys[i * nt + tid] = y;
+    dst[row] = y;
+  };
+
+  Buf<KC> A, B;
+  load(0, A);
+  int i = 0;
+  for (; i + 1 < b_s; i += 2) {
+    load(i + 1, B);
+    step(i, A);
+    if (i + 2 < b_s) load(i + 2, A);
+    step(i + 1, B);
+  }
+  if (i < b_s) step(i, A);
+}
+
+__host__ inline size_t smem_bytes(int b_s, int threads) { return (size_t)b_s * threads * 16; }
+
+}  // namespace sweep_lean

@@ -6,6 +6,7 @@ every entry point here raises -- there is no CPU fallback.
 """
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -58,8 +59,13 @@ def to_device(a, dtype=None):
 
 
 def empty(n, dtype="f64"):
+    """Output buffer.  TB_POISON=1 (set by the test suite) fills it with NaN
+    so a kernel that leaves an entry unwritten, or reads its own output
+    before writing it, cannot pass on stale memory from the allocator."""
     t = require_cuda()
     dt = {"f64": t.float64, "i32": t.int32, "i64": t.int64}[dtype]
+    if os.environ.get("TB_POISON") == "1" and dtype == "f64":
+        return t.full((int(n),), float("nan"), dtype=dt, device="cuda")
     return t.empty(int(n), dtype=dt, device="cuda")
 
 
@@ -271,6 +277,16 @@ class DevicePlan:
     def spmv(self, x, y, stream=None):
         check(LIB.tb_plan_spmv(self.handle, ptr(x), ptr(y),
                                stream if stream is not None else current_stream()))
+
+    def sweep_phase(self, forward, phase, src, dst, stream=None):
+        check(LIB.tb_plan_sweep_phase(self.handle, 1 if forward else 0, int(phase),
+                                      ptr(src), ptr(dst),
+                                      stream if stream is not None else current_stream()))
+
+    def phase_info(self, forward, phase):
+        vals = [_lib.i32() for _ in range(4)]
+        check(LIB.tb_plan_phase_info(self.handle, 1 if forward else 0, int(phase), *vals))
+        return dict(zip(("staged", "warps", "grid", "max_slots"), (v.value for v in vals)))
 
     def barriers_per_sweep(self):
         v = _lib.i64()

@@ -238,6 +238,10 @@ def level_schedule(tri: CsrMatrix, forward):
     nl = _lib.i64()
     check(LIB.tb_level_schedule(tri.n, ptr(tri.row_ptr), ptr(tri.col_idx),
                                 1 if forward else 0, ptr(level), nl))
+    if not forward:
+        # backward sweeps run their phases last-to-first (like the color
+        # phases of MC / BMC), so level 0 must be the LAST phase
+        level = nl.value - 1 - level
     phase_ptr, rows = _group(level, nl.value)
     return phase_ptr, None, rows
 

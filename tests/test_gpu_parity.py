@@ -125,9 +125,13 @@ def test_pcg_matches_reference(P, name, ordering):
     assert rep.barrier_total == int(g[f"pcg_{ordering}_barriers"])
     h = np.asarray(rep.residual_history)
     href = g[f"pcg_{ordering}_hist"]
-    m = min(h.shape[0], href.shape[0])
+    # the reference's own alignment rule (src/solver.py:216-221): common
+    # prefix minus the final two entries, where one run may already have
+    # dived below tol / hit the rounding floor
+    m = max(min(h.shape[0], href.shape[0]) - 2, 0)
     assert h[0] == href[0]
-    assert np.max(np.abs(h[:m] - href[:m]) / np.maximum(href[:m], 1e-300)) <= HIST_TOL
+    if m:
+        assert np.max(np.abs(h[:m] - href[:m]) / np.maximum(href[:m], 1e-300)) <= HIST_TOL
     key = f"pcg_{ordering}_x"
     if key in g:
         assert rel_err(x, g[key]) <= X_TOL
