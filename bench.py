@@ -7,15 +7,21 @@
 Workload (BASELINE.json configs[1]): 3-D variable-coefficient 7-point
 diffusion on 128^3, HBMC b_s=8, w=32, fp64, synthetic seeded inputs
 (SURVEY.md Appendix B).  One "step" = one preconditioner application
-z = (L L^T)^-1 r on the device (forward + backward HBMC sweep), inputs
-resident in HBM, L2 flushed (256 MiB write) before every step.
+z = (L L^T)^-1 r on the device (forward + backward HBMC sweep, all color
+phases), inputs resident in HBM.
+
+Timing: CUDA events on the launching stream, created up front; every timed
+step is enqueued without a host synchronisation (so host launch overhead
+never sits inside a timed window) and is preceded by an L2 flush that READS
+256 MiB (> the 126 MB L2; a write flush would leave dirty lines whose
+write-back lands in the timed kernel).
 
 value    = algorithmic bytes of the two sweeps (2 * (12 nnz_L + 32 N), SURVEY
-           8(d)) x steps x ranks / max-over-ranks device time.
+           8(d)) x steps x ranks / max-over-ranks summed device time.
 e2e      = the same through the public API with host buffers: pinned host r
            -> device, fwd+bwd, z -> pinned host, copies inside the timed region.
-roofline = the sweep kernel (sell_sweep, one launch per color): algorithmic
-           bytes per launch / CUDA-event launch duration vs MEASURED_PEAKS.json.
+roofline = the sweep kernel (one launch per color phase): algorithmic bytes
+           of the launch / its CUDA-event duration, vs MEASURED_PEAKS.json.
 iccg     = full PCG solve to 1e-7 on the device (one CUDA-graph launch).
 cpu_baseline = the CPU oracle port of the reference path (oracle/), all host
            threads, bounded sample of the same sweep workload (rank 0, N=1).
@@ -85,7 +91,7 @@ class ClockSampler:
                     self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -98,8 +104,8 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
-                    "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": ["nvidia-smi unavailable"], "samples": 0}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -162,12 +168,34 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+class Timer:
+    """Enqueue-only event timing on one stream (no host syncs inside)."""
+
+    def __init__(self, torch, stream, n):
+        self.t = torch
+        self.stream = stream
+        self.ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(n)]
+        self.i = 0
+
+    def start(self):
+        self.ev[self.i][0].record(self.stream)
+
+    def stop(self):
+        self.ev[self.i][1].record(self.stream)
+        self.i += 1
+
+    def times_ms(self):
+        self.t.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in self.ev[:self.i]]
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_1908_00741_b200 as P
-    from paper_1908_00741_b200 import _lib, solver
+    from paper_1908_00741_b200 import solver
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -175,20 +203,26 @@ def run_ours(args, rank, world, local_rank):
     cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
     t0 = time.perf_counter()
     setup = solver.prepare(a, b, cfg)
+    t_host = time.perf_counter() - t0
     solver.attach_plan(setup, cfg)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
-    plan, hl, sf = setup.plan, setup.layout, setup.factor
+    plan, hl = setup.plan, setup.layout
     n_pad = hl.n_pad
     nnz_l = int((a.nnz - a.n) // 2)   # strictly-lower nonzeros of A (= of L)
-    S = sweep_bytes(nnz_l, a.n)
-    step_bytes = 2 * S
+    step_bytes = 2 * sweep_bytes(nnz_l, a.n)
 
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
-    flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    flush_src = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    flush_dst = torch.empty((), dtype=torch.float64, device=dev)
+
+    def flush():
+        torch.sum(flush_src, dim=0, out=flush_dst)
+
     r = torch.from_numpy(np.random.default_rng(0).standard_normal(n_pad)).to(dev)
     z = torch.empty_like(r)
+    y = torch.empty_like(r)
 
     def barrier():
         if world > 1:
@@ -197,52 +231,56 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- device-resident steps (value)
     for _ in range(args.warmup):
-        flush.zero_()
+        flush()
         plan.precond(r, z, sptr)
     barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    tm = Timer(torch, stream, args.steps)
     with ClockSampler(local_rank) as clk:
-        for e0, e1 in ev:
-            flush.zero_()
-            e0.record(stream)
+        for _ in range(args.steps):
+            flush()
+            tm.start()
             plan.precond(r, z, sptr)
-            e1.record(stream)
-        barrier()
-    dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+            tm.stop()
+        step_ms = tm.times_ms()
+    barrier()
+    dev_ms = sum(step_ms)
     launches = 2 * hl.n_c * args.steps
 
     # ---------------- per-launch timing of the sweep kernel (roofline)
-    y = torch.empty_like(r)
-    rows_per_lvl1 = bs * w
+    span = bs * w
     lower_counts = np.diff(P.precond._strict_tri(setup.a_sys).row_ptr)
     upper_counts = np.diff(P.precond._strict_tri(setup.a_sys, upper=True).row_ptr)
     real = np.zeros(n_pad, dtype=bool)
     real[hl.real_positions] = True
-    kernel_info = [dict(plan.phase_info(fw, c), forward=fw, color=c)
-                   for fw in (True, False) for c in range(hl.n_c)]
-    per_launch = []   # (algorithmic bytes, start event, end event)
-    for rep_i in range(args.warmup + args.steps):
-        flush.zero_()
-        for direction in (True, False):
-            order = range(hl.n_c) if direction else range(hl.n_c - 1, -1, -1)
-            for c in order:
-                k0, k1 = int(hl.color_lvl1_ranges[c]), int(hl.color_lvl1_ranges[c + 1])
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                if direction:
-                    plan.sweep_phase(True, c, r, y, sptr)
-                else:
-                    plan.sweep_phase(False, c, y, z, sptr)
-                e1.record(stream)
-                if rep_i >= args.warmup:
-                    lo, hi = k0 * rows_per_lvl1, k1 * rows_per_lvl1
-                    cnt = (lower_counts if direction else upper_counts)[lo:hi]
-                    nb = 12 * int(cnt.sum()) + 32 * int(real[lo:hi].sum())
-                    per_launch.append((nb, e0, e1))
-    torch.cuda.synchronize()
-    tot_b = sum(p[0] for p in per_launch)
-    tot_ms = sum(p[1].elapsed_time(p[2]) for p in per_launch)
+    phases = []
+    for fw in (True, False):
+        for c in (range(hl.n_c) if fw else range(hl.n_c - 1, -1, -1)):
+            k0, k1 = int(hl.color_lvl1_ranges[c]), int(hl.color_lvl1_ranges[c + 1])
+            cnt = (lower_counts if fw else upper_counts)[k0 * span:k1 * span]
+            nb = 12 * int(cnt.sum()) + 32 * int(real[k0 * span:k1 * span].sum())
+            phases.append((fw, c, nb))
+    tl = Timer(torch, stream, len(phases) * (args.warmup + args.steps))
+    for _ in range(args.warmup + args.steps):
+        for fw, c, nb in phases:
+            flush()
+            tl.start()
+            if fw:
+                plan.sweep_phase(True, c, r, y, sptr)
+            else:
+                plan.sweep_phase(False, c, y, z, sptr)
+            tl.stop()
+    lt = tl.times_ms()[len(phases) * args.warmup:]
+    per_phase = []
+    for q, (fw, c, nb) in enumerate(phases):
+        ts = lt[q::len(phases)]
+        info = plan.phase_info(fw, c)
+        per_phase.append({"sweep": "fwd" if fw else "bwd", "color": c,
+                          "kernel": {0: "simple", 1: "staged", 2: "ring", 3: "reg",
+                                     4: "lean", 5: "cta", 6: "async"}[info["staged"]],
+                          "bytes": nb, "avg_us": 1e3 * sum(ts) / len(ts),
+                          "GBps": nb / (sum(ts) / len(ts) / 1e3) / 1e9})
+    tot_b = sum(p["bytes"] for p in per_phase) * args.steps
+    tot_ms = sum(lt)
     peak, peak_src = load_peaks()
     achieved = tot_b / (tot_ms / 1e3) / 1e9
 
@@ -256,31 +294,29 @@ def run_ours(args, rank, world, local_rank):
         plan.precond(r_dev, z_dev, sptr)
         z_host.copy_(z_dev, non_blocking=True)
     barrier()
-    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    for e0, e1 in ee:
-        flush.zero_()
-        e0.record(stream)
+    te = Timer(torch, stream, args.steps)
+    for _ in range(args.steps):
+        flush()
+        te.start()
         r_dev.copy_(r_host, non_blocking=True)
         plan.precond(r_dev, z_dev, sptr)
         z_host.copy_(z_dev, non_blocking=True)
-        e1.record(stream)
+        te.stop()
+    e2e_ms = sum(te.times_ms())
     barrier()
-    e2e_ms = sum(e0.elapsed_time(e1) for e0, e1 in ee)
 
     # ---------------- ICCG time-to-solution on the device
     b_dev = torch.from_numpy(setup.b_sys).to(dev)
     x_dev = torch.empty_like(b_dev)
-    rep0, _ = plan.pcg(b_dev, x_dev, cfg.tol, cfg.max_iters)   # warm-up (graph build)
+    plan.pcg(b_dev, x_dev, cfg.tol, cfg.max_iters, sptr)   # warm-up (graph build)
     solves = []
     for _ in range(3):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        flush()
+        ts = Timer(torch, stream, 1)
+        ts.start()
         rep, hist = plan.pcg(b_dev, x_dev, cfg.tol, cfg.max_iters, sptr)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        solves.append(e0.elapsed_time(e1))
+        ts.stop()
+        solves.append(ts.times_ms()[0])
     x_sys = x_dev.cpu().numpy()
     x = x_sys[setup.old_positions]
     err = float(np.linalg.norm(x - xs) / np.linalg.norm(xs))
@@ -289,7 +325,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        xh, rep_h, _ = solver.solve_on_device(setup, cfg)
+        solver.solve_on_device(setup, cfg)
         t_e2e_solve.append(time.perf_counter() - t0)
 
     # ---------------- max over ranks
@@ -312,10 +348,10 @@ def run_ours(args, rank, world, local_rank):
             from oracle import oracle as O
             cb, _ = cpu_baseline(a, b, bs, w, min(args.steps, 10), 2, O.max_threads())
         digest = os.path.join(HERE, "tests", "golden", f"config{args.config}_digest.json")
-        ref_iters = None
+        ref = {}
         if os.path.exists(digest):
             with open(digest) as fh:
-                ref_iters = json.load(fh)["hbmc"]["iterations"]
+                ref = json.load(fh).get("hbmc", {})
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -325,22 +361,24 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": f"config{args.config} {label} b_s={bs} w={w}",
                        "N": a.n, "n_pad": n_pad, "nnz_A": int(a.nnz), "nnz_L": nnz_l,
                        "n_c": hl.n_c, "bytes_per_step": step_bytes,
-                       "l2": "flushed (256 MiB write) before every timed step",
+                       "l2": "flushed before every timed step (256 MiB read)",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
-            "roofline": {"bound": "hbm", "kernel": "sell_sweep (fwd+bwd, per color launch)",
+            "roofline": {"bound": "hbm", "kernel": "HBMC sweep (one launch per color phase)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
-                         "launches": len(per_launch),
-                         "avg_launch_us": 1e3 * tot_ms / max(1, len(per_launch)),
-                         "algorithmic_bytes_per_launch": tot_b / max(1, len(per_launch)),
-                         "traffic": None, "phases": kernel_info},
+                         "launches": len(lt), "avg_launch_us": 1e3 * tot_ms / max(1, len(lt)),
+                         "algorithmic_bytes_per_launch": tot_b / max(1, len(lt)),
+                         "traffic": None, "phases": per_phase},
             "cpu_baseline": cb,
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_pad, "d2h_bytes_per_step": 8 * n_pad,
                     "ms_per_step": e2e_ms_max / args.steps},
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "iccg": {"iterations": int(rep.iterations), "reference_iterations": ref_iters,
+            "iccg": {"iterations": int(rep.iterations),
+                     "reference_iterations": ref.get("iterations"),
+                     "reference_cpu_solve_s": ref.get("time_solve_s"),
+                     "reference_cpu_threads": ref.get("threads"),
                      "converged": bool(rep.converged),
                      "time_to_solution_ms": min(solves),
                      "ms_per_iteration": min(solves) / max(1, rep.iterations),
@@ -348,7 +386,8 @@ def run_ours(args, rank, world, local_rank):
                      "host_syncs": int(rep.host_syncs),
                      "rel_err_vs_xstar": err,
                      "e2e_solve_ms": 1e3 * min(t_e2e_solve),
-                     "setup_s": t_setup, "generate_s": t_gen},
+                     "setup_host_s": t_host, "setup_total_s": t_setup,
+                     "generate_s": t_gen},
             "spmv_bytes_per_call": spmv_bytes(int(a.nnz), a.n),
         }
         print(json.dumps(line), flush=True)

@@ -194,17 +194,34 @@ __global__ void __launch_bounds__(kBlock)
               double *partials, PcgState *st) {
   if (DOT && st->done) return;
   double part = 0.0;
+  constexpr int CH = 8;  // slots whose loads / gathers are in flight together
   for (long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x; row < n;
        row += (long long)gridDim.x * blockDim.x) {
     const long long s = row / w;
     const int j = (int)(row - s * w);
-    long long off = slice_ptr[s] + j;
+    const long long off = slice_ptr[s] + j;
     const int len = slice_len[s];
+    const double xr = DOT ? __ldg(x + row) : 0.0;
     double acc = 0.0;
-    for (int t = 0; t < len; ++t, off += w)
-      acc = __dadd_rn(acc, __dmul_rn(val[off], x[col[off]]));
+    for (int t0 = 0; t0 < len; t0 += CH) {
+      const int *cp = col + off + (long long)t0 * w;
+      const double *vp = val + off + (long long)t0 * w;
+      int c[CH];
+      double v[CH], xv[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const bool in = t0 + u < len;
+        c[u] = in ? __ldg(cp + (long long)u * w) : 0;
+        v[u] = in ? __ldg(vp + (long long)u * w) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < CH; ++u) xv[u] = t0 + u < len ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < CH; ++u)
+        if (t0 + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    }
     out[row] = acc;
-    if (DOT) part += x[row] * acc;
+    if (DOT) part += xr * acc;
   }
   if (DOT)
     grid_reduce(part, partials, &st->counter[0], [st](double pap) {
@@ -281,6 +298,23 @@ __global__ void __launch_bounds__(kBlock)
   });
 }
 
+// Grid-stride loops below process 4 strided elements per trip with all their
+// loads issued together (fixed order => deterministic partial sums).
+#define TB_GRID_STRIDE4(BODY)                                                  \
+  {                                                                            \
+    const long long stride = (long long)gridDim.x * blockDim.x;               \
+    long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;          \
+    for (; i0 + 3 * stride < n; i0 += 4 * stride) {                           \
+      _Pragma("unroll") for (int u = 0; u < 4; ++u) {                          \
+        const long long i = i0 + u * stride;                                   \
+        BODY                                                                   \
+      }                                                                        \
+    }                                                                          \
+    for (long long i = i0; i < n; i += stride) {                               \
+      BODY                                                                     \
+    }                                                                          \
+  }
+
 // x += alpha p; r -= alpha ap; rel = ||r|| / ||b|| (src/solver.py:178-186).
 __global__ void __launch_bounds__(kBlock)
     cg_update_xr(long long n, const double *__restrict__ p,
@@ -290,13 +324,12 @@ __global__ void __launch_bounds__(kBlock)
   if (st->done) return;
   const double alpha = st->alpha;
   double part = 0.0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
+  TB_GRID_STRIDE4({
     x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
     const double ri = __dsub_rn(r[i], __dmul_rn(alpha, ap[i]));
     r[i] = ri;
     part += ri * ri;
-  }
+  })
   grid_reduce(part, partials, &st->counter[2], [st, hist](double rr) {
     const long long j = st->iter + 1;
     const double rel = sqrt(rr) / st->bnorm;
@@ -321,12 +354,11 @@ __global__ void __launch_bounds__(kBlock)
           double *partials, PcgState *st) {
   if (st->done) return;
   double part = 0.0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
+  TB_GRID_STRIDE4({
     const double zi = z[i];
     part += r[i] * zi;
     if (FIRST) p[i] = zi;
-  }
+  })
   grid_reduce(part, partials, &st->counter[3], [st](double rz) {
     if (FIRST) {
       st->rz = rz;
@@ -343,9 +375,7 @@ __global__ void __launch_bounds__(kBlock)
                 double *__restrict__ p, const PcgState *st) {
   if (st->done) return;
   const double beta = st->beta;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+  TB_GRID_STRIDE4({ p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i])); })
 }
 
 // ------------------------------------------------------------ helpers
@@ -355,9 +385,9 @@ inline unsigned grid_for(long long n, int per_block = kBlock) {
   return (unsigned)g;
 }
 
-inline unsigned reduce_grid(long long n) {
-  // Fixed for a given n: up to 4 CTAs per SM-ish worth of work, capped.
-  long long g = (n + kBlock * 4 - 1) / (kBlock * 4);
+inline unsigned reduce_grid(long long n, int per_thread = 4) {
+  // Fixed for a given n (=> fixed summation tree), capped at kMaxPartials.
+  long long g = (n + (long long)kBlock * per_thread - 1) / ((long long)kBlock * per_thread);
   if (g < 1) g = 1;
   if (g > kMaxPartials) g = kMaxPartials;
   return (unsigned)g;
@@ -568,7 +598,7 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
     L.n_tasks = (L.k1 - L.k0 + G - 1) / G;
     if (force_simple || L.n_tasks <= 0) continue;
     const bool idx32 = pl->n <= 0x7fffffffLL && h.slice_ptr[h.n_slices] <= 0x7fffffffLL;
-    if ((!mode || !strcmp(mode, "async")) && idx32) {
+    if (mode && !strcmp(mode, "async") && idx32) {
       // ---- cp.async ring, thread per lane
       long long lmax = 0;
       for (long long sid = L.k0 * b_s; sid < L.k1 * b_s; ++sid)
@@ -588,7 +618,7 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
         continue;
       }
     }
-    if ((!mode || !strcmp(mode, "cta")) && idx32 && b_s * w <= 1024) {
+    if (mode && !strcmp(mode, "cta") && idx32 && b_s * w <= 1024) {
       // ---- two-pass CTA kernel
       long long lmax = 0;
       for (long long sid = L.k0 * b_s; sid < L.k1 * b_s; ++sid)
@@ -890,7 +920,7 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
     return fail(TB_EINVAL, "plan has no matrix A (preconditioner-only plan)");
   if (pl->spmv_format == TB_SPMV_SELL) {
     if (dot)
-      spmv_sell<true><<<reduce_grid(n), kBlock, 0, s>>>(
+      spmv_sell<true><<<reduce_grid(n, 1), kBlock, 0, s>>>(
           n, pl->A.slice_ptr, pl->A.slice_len, pl->A.col, pl->A.val,
           (int)pl->A.width, x, out, pl->partials, pl->st);
     else
@@ -922,7 +952,7 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   if ((rc = launch_forward(pl, pl->r, pl->y, s, pl->st, nl))) return rc;
   if ((rc = launch_backward(pl, pl->y, pl->z, s, pl->st, nl))) return rc;
   cg_rz<false><<<rg, kBlock, 0, s>>>(n, pl->r, pl->z, pl->p, pl->partials, pl->st);
-  cg_update_p<<<grid_for(n), kBlock, 0, s>>>(n, pl->z, pl->p, pl->st);
+  cg_update_p<<<reduce_grid(n), kBlock, 0, s>>>(n, pl->z, pl->p, pl->st);
   *nl += 2;
   CU(cudaGetLastError());
   return TB_OK;
@@ -1221,7 +1251,14 @@ extern "C" int tb_plan_spmv(tb_plan *pl, const double *x, double *y, void *strea
 extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
                       int64_t max_iters, int64_t check_every, void *stream,
                       tb_pcg_report *rep, double *history_host) {
-  (void)check_every;  // the loop is device-resident: no host polling
+  // check_every == 0: the whole loop is one CUDA graph (device-side
+  // convergence test).  check_every > 0 (or env TB_PCG_NOGRAPH=<n>): plain
+  // launches, the host polls the device state every check_every iterations
+  // (profilers cannot see inside conditional graph nodes).
+  {
+    const int env_batch = env_int("TB_PCG_NOGRAPH", 0);
+    if (env_batch > 0) check_every = env_batch;
+  }
   if (!pl || !rep || !history_host) return fail(TB_EINVAL, "pcg: null argument");
   if (!(tol > 0.0) || max_iters < 1) return fail(TB_EINVAL, "pcg: bad tol / max_iters");
   CU(cudaSetDevice(pl->device));
@@ -1241,17 +1278,36 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
   hs.tol = tol;
   hs.max_iters = max_iters;
   hs.loop = h;
-  hs.has_loop = has;
+  hs.has_loop = check_every > 0 ? 0 : has;
   CU(cudaMemcpy(pl->st, &hs, sizeof(PcgState), cudaMemcpyHostToDevice));
-  if (!pl->gexec || pl->g_b != b || pl->g_x != x || pl->g_hist_cap != pl->hist_cap) {
-    int rc = build_graph(pl, b, x);
-    if (rc) return rc;
+  int rc;
+  long long polled_launches = 0, polls = 0;
+  if (check_every > 0) {
+    if ((rc = sync_in(pl, stream))) return rc;
+    if ((rc = launch_prologue(pl, b, x, pl->stream, &polled_launches))) return rc;
+    for (;;) {
+      for (int64_t q = 0; q < check_every; ++q)
+        if ((rc = launch_iteration(pl, x, pl->stream, &polled_launches))) return rc;
+      CU(cudaMemcpyAsync(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost, pl->stream));
+      CU(cudaStreamSynchronize(pl->stream));
+      ++polls;
+      if (hs.done) break;
+    }
+    // restore the graph-loop fields for the next graph run
+    PcgState tmp = hs;
+    tmp.loop = h;
+    tmp.has_loop = has;
+    CU(cudaMemcpy(pl->st, &tmp, sizeof(PcgState), cudaMemcpyHostToDevice));
+  } else {
+    if (!pl->gexec || pl->g_b != b || pl->g_x != x || pl->g_hist_cap != pl->hist_cap) {
+      rc = build_graph(pl, b, x);
+      if (rc) return rc;
+    }
+    if ((rc = sync_in(pl, stream))) return rc;
+    CU(cudaGraphLaunch(pl->gexec, pl->stream));
+    CU(cudaMemcpyAsync(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost, pl->stream));
+    CU(cudaStreamSynchronize(pl->stream));
   }
-  int rc = sync_in(pl, stream);
-  if (rc) return rc;
-  CU(cudaGraphLaunch(pl->gexec, pl->stream));
-  CU(cudaMemcpyAsync(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost, pl->stream));
-  CU(cudaStreamSynchronize(pl->stream));
   if ((rc = sync_out(pl, stream))) return rc;
   const long long iters = hs.iter;
   CU(cudaMemcpy(history_host, pl->hist, sizeof(double) * (size_t)(iters + 1),
@@ -1265,6 +1321,10 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
   // body runs iters times on success, iters+1 times on a breakdown / max-iter exit
   const long long bodies = hs.bnorm == 0.0 ? 0 : (hs.status ? iters + 1 : iters);
   rep->kernel_launches = pl->launches_prologue + bodies * pl->launches_per_iter;
+  if (check_every > 0) {
+    rep->kernel_launches = polled_launches;
+    rep->host_syncs = polls;
+  }
   if (hs.status == TB_ECG_BREAKDOWN)
     return fail(TB_ECG_BREAKDOWN, "p.Ap = %.6g <= 0 at iteration %lld", hs.bd_val,
                 (long long)hs.bd_iter);

@@ -21,6 +21,10 @@
 
 #pragma once
 
+#ifndef TB_LEAN_MINB
+#define TB_LEAN_MINB 1
+#endif
+
 namespace sweep_lean {
 
 template <int KC>
@@ -32,7 +36,7 @@ struct Buf {
 
 // W > 0: compile-time slice width; W == 0: runtime w
 template <bool FWD, int KC, int W>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, TB_LEAN_MINB)
     sweep_kernel(const long long *__restrict__ slice_ptr, const int *__restrict__ slice_len,
                  const int *__restrict__ col, const double *__restrict__ val,
                  const double *__restrict__ inv_d, const double *__restrict__ src,
@@ -76,6 +80,7 @@ __global__ void __launch_bounds__(256)
     b.idg = __ldg(inv_d + row);
   };
 
+  const double *dstc = dst;  // gathers read earlier-phase rows only
   auto step = [&](int i, const Buf<KC> &b) {
     const int l = FWD ? i : b_s - 1 - i;
     const int row = blk0 + l * w + j;
@@ -84,19 +89,19 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int u = 0; u < KC; ++u) {
       const bool inblk = (unsigned)(b.c[u] - blk0) < uspan;
-      x[u] = inblk ? 0.0 : __ldg(dst + b.c[u]);
+      x[u] = inblk ? 0.0 : __ldg(dstc + b.c[u]);
     }
     double y = b.rhs;
+    // branch-free slot update: the shared-memory read is clamped in range
+    // and selected away for cross / padding slots
     auto update = [&](int cc, double vv, double xcross) {
-      double xv = xcross;
-      if ((unsigned)(cc - blk0) < uspan) {
-        if (cc == row) {
-          xv = y;
-        } else {
-          const int lp = (cc - blk0) / w;
-          xv = ys[(FWD ? lp : b_s - 1 - lp) * nt + tid];
-        }
-      }
+      const unsigned rel = (unsigned)(cc - blk0);
+      const bool inblk = rel < uspan;
+      unsigned lp = W > 0 ? rel / (unsigned)W : rel / (unsigned)w;
+      lp = lp < (unsigned)b_s ? lp : 0u;
+      const double ysv = ys[(FWD ? (int)lp : b_s - 1 - (int)lp) * nt + tid];
+      const double xin = cc == row ? y : ysv;
+      const double xv = inblk ? xin : xcross;
       y = __dsub_rn(y, __dmul_rn(vv, xv));
     };
 #pragma unroll
