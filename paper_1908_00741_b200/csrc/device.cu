@@ -40,6 +40,7 @@ using tb::fail;
 #include "sweep_reg.cuh"
 #include "sweep_ring.cuh"
 #include "sweep_tma.cuh"
+#include "persist.cuh"
 
 #define CU(call)                                                          \
   do {                                                                    \
@@ -378,6 +379,108 @@ __global__ void __launch_bounds__(kBlock)
   TB_GRID_STRIDE4({ p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i])); })
 }
 
+// ------------------------------------------------------------ persistent
+// Whole preconditioner application (mode 0) or whole PCG solve (mode 1) in
+// one cooperative launch; see persist.cuh.  Writes the final PcgState.
+template <int KC>
+__global__ void __launch_bounds__(persist::kThreads, 2) pcg_persistent(persist::Params P) {
+  extern __shared__ __align__(16) double psm[];
+  const int T = blockDim.x, b_s = P.b_s;
+  double *ys = psm;
+  int *offs = (int *)(ys + (size_t)b_s * T);
+  int *lens = offs + (size_t)b_s * T;
+  double *sh = (double *)(lens + (size_t)b_s * T + (((size_t)b_s * T) & 1));
+  PcgState *st = (PcgState *)P.state;
+  const int gthreads = gridDim.x * blockDim.x;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = P.n;
+  if (P.mode == 0) {
+    persist::sweep<true, KC>(P, P.pre_src, P.y, ys, offs, lens);
+    persist::sweep<false, KC>(P, P.y, P.pre_dst, ys, offs, lens);
+    return;
+  }
+  const double tol = st->tol;
+  const long long max_iters = st->max_iters;
+  // x = 0; r = b; bnorm = ||b||  (src/solver.py:159-167)
+  double part = 0.0;
+  for (int i = gtid; i < n; i += gthreads) {
+    const double bi = P.b[i];
+    P.x[i] = 0.0;
+    P.r[i] = bi;
+    part += bi * bi;
+  }
+  const double bnorm = sqrt(persist::grid_sum(P, part, 0, sh));
+  if (bnorm == 0.0) {
+    if (gtid == 0) {
+      P.hist[0] = 0.0;
+      st->bnorm = 0.0;
+      st->iter = 0;
+      st->converged = 1;
+      st->status = TB_OK;
+      st->done = 1;
+    }
+    return;
+  }
+  if (gtid == 0) P.hist[0] = 1.0;
+  persist::sweep<true, KC>(P, P.r, P.y, ys, offs, lens);
+  persist::sweep<false, KC>(P, P.y, P.z, ys, offs, lens);
+  part = 0.0;
+  for (int i = gtid; i < n; i += gthreads) {
+    const double zi = __ldcg(P.z + i);
+    part += __ldcg(P.r + i) * zi;
+    P.p[i] = zi;
+  }
+  double rz = persist::grid_sum(P, part, 1, sh);
+  long long j = 1, iters = 0;
+  int converged = 0, status = TB_OK;
+  double bd_val = 0.0, rel = 1.0;
+  for (; j <= max_iters; ++j) {
+    const double pap = persist::grid_sum(P, persist::spmv_dot(P), 2, sh);
+    if (pap <= 0.0) {  // src/solver.py:176-177
+      status = TB_ECG_BREAKDOWN;
+      bd_val = pap;
+      break;
+    }
+    const double alpha = rz / pap;
+    part = 0.0;
+    for (int i = gtid; i < n; i += gthreads) {
+      P.x[i] = __dadd_rn(P.x[i], __dmul_rn(alpha, __ldcg(P.p + i)));
+      const double ri = __dsub_rn(P.r[i], __dmul_rn(alpha, __ldcg(P.ap + i)));
+      P.r[i] = ri;
+      part += ri * ri;
+    }
+    rel = sqrt(persist::grid_sum(P, part, 3, sh)) / bnorm;
+    if (gtid == 0) P.hist[j] = rel;
+    iters = j;
+    if (rel < tol) {
+      converged = 1;
+      break;
+    }
+    if (j == max_iters) break;
+    persist::sweep<true, KC>(P, P.r, P.y, ys, offs, lens);
+    persist::sweep<false, KC>(P, P.y, P.z, ys, offs, lens);
+    part = 0.0;
+    for (int i = gtid; i < n; i += gthreads) part += __ldcg(P.r + i) * __ldcg(P.z + i);
+    const double rzn = persist::grid_sum(P, part, 1, sh);
+    const double beta = rzn / rz;
+    rz = rzn;
+    for (int i = gtid; i < n; i += gthreads)
+      P.p[i] = __dadd_rn(__ldcg(P.z + i), __dmul_rn(beta, __ldcg(P.p + i)));
+    persist::grid_sync(P);
+  }
+  if (gtid == 0) {
+    st->bnorm = bnorm;
+    st->iter = iters;
+    st->rel = rel;
+    st->converged = converged;
+    st->status = status;
+    st->bd_iter = status ? j : 0;
+    st->bd_val = bd_val;
+    st->rz = rz;
+    st->done = 1;
+  }
+}
+
 // ------------------------------------------------------------ helpers
 inline unsigned grid_for(long long n, int per_block = kBlock) {
   long long g = (n + per_block - 1) / per_block;
@@ -558,6 +661,13 @@ struct tb_plan {
   double *g_x = nullptr;
   long long g_hist_cap = 0;
   long long launches_prologue = 0, launches_per_iter = 0;
+  // persistent cooperative path (HBMC + SELL A, 32-bit indexing)
+  bool persist_ok = false, persist_pcg_ok = false;
+  int persist_kc = 0, persist_grid = 0;
+  size_t persist_smem = 0;
+  int *color_lvl1_dev = nullptr;
+  unsigned *bar = nullptr;  // [count, generation]
+  double *ppartials = nullptr;
 };
 
 namespace {
@@ -1041,6 +1151,108 @@ int build_graph(tb_plan *pl, const double *b, double *x) {
   return TB_OK;
 }
 
+// ------------------------------------------------------------ persistent host side
+using PersistFn = void (*)(persist::Params);
+
+PersistFn persist_fn(int kc) {
+  switch (kc) {
+    case 2: return pcg_persistent<2>;
+    case 4: return pcg_persistent<4>;
+    case 6: return pcg_persistent<6>;
+    default: return pcg_persistent<8>;
+  }
+}
+
+// Decide whether the persistent kernel applies and size its cooperative grid.
+int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
+  pl->persist_ok = false;
+  const char *e = getenv("TB_PERSIST");
+  if (e && !strcmp(e, "0")) return TB_OK;
+  if (pl->precond_kind != TB_PRECOND_HBMC || pl->n > 0x7fffffffLL) return TB_OK;
+  if (d->L_sell.slice_ptr[d->L_sell.n_slices] > 0x7fffffffLL ||
+      d->U_sell.slice_ptr[d->U_sell.n_slices] > 0x7fffffffLL)
+    return TB_OK;
+  if (d->spmv_format == TB_SPMV_SELL &&
+      d->A_sell.slice_ptr[d->A_sell.n_slices] > 0x7fffffffLL)
+    return TB_OK;
+  long long lmax = 0;
+  for (long long s = 0; s < d->L_sell.n_slices; ++s)
+    lmax = d->L_sell.slice_len[s] > lmax ? d->L_sell.slice_len[s] : lmax;
+  for (long long s = 0; s < d->U_sell.n_slices; ++s)
+    lmax = d->U_sell.slice_len[s] > lmax ? d->U_sell.slice_len[s] : lmax;
+  const int kc = lmax <= 2 ? 2 : (lmax <= 4 ? 4 : (lmax <= 6 ? 6 : 8));
+  const size_t T = persist::kThreads;
+  const size_t smem = (size_t)pl->b_s * T * 16 + 8 + 33 * 8 + 64;
+  int v = 0;
+  CU(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
+  if (smem > (size_t)v) return TB_OK;
+  PersistFn fn = persist_fn(kc);
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)T, smem));
+  if (per_sm < 1) return TB_OK;
+  if (per_sm > 2) per_sm = 2;
+  pl->persist_kc = kc;
+  pl->persist_smem = smem;
+  pl->persist_grid = per_sm * pl->num_sms;
+  std::vector<int> cl(pl->color_lvl1.begin(), pl->color_lvl1.end());
+  int rc;
+  if ((rc = upload(&pl->color_lvl1_dev, cl.data(), (long long)cl.size()))) return rc;
+  CU(cudaMalloc((void **)&pl->bar, 2 * sizeof(unsigned)));
+  CU(cudaMemset(pl->bar, 0, 2 * sizeof(unsigned)));
+  CU(cudaMalloc((void **)&pl->ppartials, sizeof(double) * persist::kSlots * pl->persist_grid));
+  pl->persist_ok = true;
+  pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
+  return TB_OK;
+}
+
+// mode 0: z = M r (src -> dst); mode 1: whole PCG (b, x; state preset).
+int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, const double *b,
+                      double *x, cudaStream_t s) {
+  persist::Params P;
+  memset(&P, 0, sizeof(P));
+  P.mode = mode;
+  P.n = (int)pl->n;
+  P.w = (int)pl->w;
+  P.b_s = (int)pl->b_s;
+  P.n_c = (int)pl->n_c;
+  P.color_lvl1 = pl->color_lvl1_dev;
+  P.Lsp = pl->L.slice_ptr;
+  P.Usp = pl->U.slice_ptr;
+  P.Lsl = pl->L.slice_len;
+  P.Usl = pl->U.slice_len;
+  P.Lcol = pl->L.col;
+  P.Ucol = pl->U.col;
+  P.Lval = pl->L.val;
+  P.Uval = pl->U.val;
+  P.inv_d = pl->inv_d;
+  P.Asp = pl->A.slice_ptr;
+  P.Asl = pl->A.slice_len;
+  P.Acol = pl->A.col;
+  P.Aval = pl->A.val;
+  P.aw = (int)(pl->A.width > 0 ? pl->A.width : 1);
+  P.b = b;
+  P.x = x;
+  P.r = pl->r;
+  P.y = pl->y;
+  P.z = pl->z;
+  P.p = pl->p;
+  P.ap = pl->ap;
+  P.pre_src = src;
+  P.pre_dst = dst;
+  P.hist = pl->hist;
+  P.partials = pl->ppartials;
+  P.bar_count = pl->bar;
+  P.bar_gen = pl->bar + 1;
+  P.state = pl->st;
+  P.watchdog = 4000000000LL;  // ~2 s at 1.9 GHz per barrier wait
+  void *args[] = {&P};
+  CU(cudaLaunchCooperativeKernel((const void *)persist_fn(pl->persist_kc),
+                                 dim3(pl->persist_grid), dim3(persist::kThreads), args,
+                                 pl->persist_smem, s));
+  return TB_OK;
+}
+
 int sync_in(tb_plan *pl, void *stream) {
   CU(cudaEventRecord(pl->ev_in, (cudaStream_t)stream));
   CU(cudaStreamWaitEvent(pl->stream, pl->ev_in, 0));
@@ -1100,6 +1312,7 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
     }
     if ((rc = configure_sweeps(pl, d->L_sell, pl->cl_fwd))) return bail(rc);
     if ((rc = configure_sweeps(pl, d->U_sell, pl->cl_bwd))) return bail(rc);
+    if ((rc = configure_persistent(pl, d))) return bail(rc);
   } else if (d->precond_kind == TB_PRECOND_TASKS) {
     if ((rc = upload_csr(pl->Lc, d->L_csr))) return bail(rc);
     if ((rc = upload_csr(pl->Uc, d->U_csr))) return bail(rc);
@@ -1161,6 +1374,9 @@ extern "C" int tb_plan_destroy(tb_plan *pl) {
   cudaFree(pl->partials);
   cudaFree(pl->st);
   cudaFree(pl->hist);
+  cudaFree(pl->color_lvl1_dev);
+  cudaFree(pl->bar);
+  cudaFree(pl->ppartials);
   if (pl->ev_in) cudaEventDestroy(pl->ev_in);
   if (pl->ev_out) cudaEventDestroy(pl->ev_out);
   if (pl->stream) cudaStreamDestroy(pl->stream);
@@ -1204,6 +1420,8 @@ extern "C" int tb_plan_backward(tb_plan *pl, const double *y, double *z, void *s
 extern "C" int tb_plan_precond(tb_plan *pl, const double *r, double *z, void *stream) {
   if (!pl) return fail(TB_EINVAL, "null plan");
   CU(cudaSetDevice(pl->device));
+  if (pl->persist_ok)  // one cooperative launch for all color phases of both sweeps
+    return launch_persistent(pl, 0, r, z, nullptr, nullptr, (cudaStream_t)stream);
   long long nl = 0;
   int rc = launch_forward(pl, r, pl->y, (cudaStream_t)stream, nullptr, &nl);
   if (rc) return rc;
@@ -1282,7 +1500,13 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
   CU(cudaMemcpy(pl->st, &hs, sizeof(PcgState), cudaMemcpyHostToDevice));
   int rc;
   long long polled_launches = 0, polls = 0;
-  if (check_every > 0) {
+  const bool persistent = check_every <= 0 && pl->persist_ok && pl->persist_pcg_ok;
+  if (persistent) {
+    if ((rc = sync_in(pl, stream))) return rc;
+    if ((rc = launch_persistent(pl, 1, nullptr, nullptr, b, x, pl->stream))) return rc;
+    CU(cudaMemcpyAsync(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost, pl->stream));
+    CU(cudaStreamSynchronize(pl->stream));
+  } else if (check_every > 0) {
     if ((rc = sync_in(pl, stream))) return rc;
     if ((rc = launch_prologue(pl, b, x, pl->stream, &polled_launches))) return rc;
     for (;;) {
@@ -1325,6 +1549,7 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
     rep->kernel_launches = polled_launches;
     rep->host_syncs = polls;
   }
+  if (persistent) rep->kernel_launches = 1;
   if (hs.status == TB_ECG_BREAKDOWN)
     return fail(TB_ECG_BREAKDOWN, "p.Ap = %.6g <= 0 at iteration %lld", hs.bd_val,
                 (long long)hs.bd_iter);

@@ -2,8 +2,8 @@
 //
 // Same arithmetic as K/numba_backend.py:132-171, bitwise.  One thread per
 // (level-1 block k, lane j); the thread walks its b_s rows.  The walk is a
-// chain of dependent steps, so the kernel is built to keep DRAM traffic in
-// flight while each step waits on its gathers, with a short instruction
+// chain of dependent steps, so the lane chain is built to keep DRAM traffic
+// in flight while each step waits on its gathers, with a short instruction
 // stream:
 //   * all step descriptors (slice offset, length) are loaded up front into
 //     the thread's column of shared memory;
@@ -14,10 +14,15 @@
 //   * with W = 32 known at compile time every slot load is an immediate
 //     offset from one base pointer per step;
 //   * in-block operands (same lane, earlier step) are read back from the
-//     thread's results in shared memory;
+//     thread's results in shared memory (branch-free, clamped index);
 //   * 32-bit row / column / slot arithmetic (the host checks the ranges).
 // Products __dmul_rn, updates __dsub_rn, slot order = the reference's; a
 // padding slot (col == own row, v == 0) multiplies the in-progress value.
+//
+// lane_chain() is shared by the per-phase kernel below (CG = false: vectors
+// read through the read-only path, valid because every phase is its own
+// launch) and the persistent kernel of persist.cuh (CG = true: vectors that
+// other CTAs wrote inside the same launch are read with ld.global.cg).
 
 #pragma once
 
@@ -34,26 +39,23 @@ struct Buf {
   double rhs, idg;
 };
 
-// W > 0: compile-time slice width; W == 0: runtime w
-template <bool FWD, int KC, int W>
-__global__ void __launch_bounds__(256, TB_LEAN_MINB)
-    sweep_kernel(const long long *__restrict__ slice_ptr, const int *__restrict__ slice_len,
-                 const int *__restrict__ col, const double *__restrict__ val,
-                 const double *__restrict__ inv_d, const double *__restrict__ src,
-                 double *__restrict__ dst, int w_rt, int b_s, int k0, int nthreads,
-                 const int *done) {
-  // shared: ys[b_s][T] doubles | offs[b_s][T] ints | lens[b_s][T] ints
-  extern __shared__ __align__(16) double ys[];
-  if (done && *(const volatile int *)done) return;
+template <bool CG>
+__device__ __forceinline__ double ldv(const double *p) {
+  return CG ? __ldcg(p) : __ldg(p);
+}
+
+// One lane's b_s-step walk.  W > 0: compile-time slice width; W == 0: w_rt.
+// Shared memory: ys/offs/lens columns of this thread ([b_s][nt] each).
+template <bool FWD, int KC, int W, bool CG>
+__device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_ptr,
+                                           const int *__restrict__ slice_len,
+                                           const int *__restrict__ col,
+                                           const double *__restrict__ val,
+                                           const double *__restrict__ inv_d,
+                                           const double *src, double *dst, int w_rt, int b_s,
+                                           int k, int j, double *ys, int *offs, int *lens) {
   const int w = W > 0 ? W : w_rt;
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= nthreads) return;
   const int tid = threadIdx.x, nt = blockDim.x;
-  int *offs = (int *)(ys + (size_t)b_s * nt);
-  int *lens = offs + (size_t)b_s * nt;
-  const int kq = g / w;
-  const int j = g - kq * w;
-  const int k = k0 + kq;
   const int span = b_s * w;
   const int blk0 = k * span;
   const unsigned uspan = (unsigned)span;
@@ -76,11 +78,10 @@ __global__ void __launch_bounds__(256, TB_LEAN_MINB)
       b.c[u] = in ? __ldg(cp + u * w) : row;
       b.v[u] = in ? __ldg(vp + u * w) : 0.0;
     }
-    b.rhs = __ldg(src + row);
+    b.rhs = ldv<CG>(src + row);
     b.idg = __ldg(inv_d + row);
   };
 
-  const double *dstc = dst;  // gathers read earlier-phase rows only
   auto step = [&](int i, const Buf<KC> &b) {
     const int l = FWD ? i : b_s - 1 - i;
     const int row = blk0 + l * w + j;
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(256, TB_LEAN_MINB)
 #pragma unroll
     for (int u = 0; u < KC; ++u) {
       const bool inblk = (unsigned)(b.c[u] - blk0) < uspan;
-      x[u] = inblk ? 0.0 : __ldg(dstc + b.c[u]);
+      x[u] = inblk ? 0.0 : ldv<CG>(dst + b.c[u]);
     }
     double y = b.rhs;
     // branch-free slot update: the shared-memory read is clamped in range
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(256, TB_LEAN_MINB)
       for (int t = KC; t < len; ++t) {
         const int cc = __ldg(col + off + t * w);
         const double vv = __ldg(val + off + t * w);
-        const double xc = (unsigned)(cc - blk0) < uspan ? 0.0 : __ldg(dst + cc);
+        const double xc = (unsigned)(cc - blk0) < uspan ? 0.0 : ldv<CG>(dst + cc);
         update(cc, vv, xc);
       }
     }
@@ -131,6 +132,26 @@ __global__ void __launch_bounds__(256, TB_LEAN_MINB)
     step(i + 1, B);
   }
   if (i < b_s) step(i, A);
+}
+
+template <bool FWD, int KC, int W>
+__global__ void __launch_bounds__(256, TB_LEAN_MINB)
+    sweep_kernel(const long long *__restrict__ slice_ptr, const int *__restrict__ slice_len,
+                 const int *__restrict__ col, const double *__restrict__ val,
+                 const double *__restrict__ inv_d, const double *__restrict__ src,
+                 double *__restrict__ dst, int w_rt, int b_s, int k0, int nthreads,
+                 const int *done) {
+  // shared: ys[b_s][T] doubles | offs[b_s][T] ints | lens[b_s][T] ints
+  extern __shared__ __align__(16) double ys[];
+  if (done && *(const volatile int *)done) return;
+  const int w = W > 0 ? W : w_rt;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nthreads) return;
+  int *offs = (int *)(ys + (size_t)b_s * blockDim.x);
+  int *lens = offs + (size_t)b_s * blockDim.x;
+  const int kq = g / w;
+  lane_chain<FWD, KC, W, false>(slice_ptr, slice_len, col, val, inv_d, src, dst, w, b_s,
+                                k0 + kq, g - kq * w, ys, offs, lens);
 }
 
 __host__ inline size_t smem_bytes(int b_s, int threads) { return (size_t)b_s * threads * 16; }
