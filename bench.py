@@ -279,9 +279,20 @@ def run_ours(args, rank, world, local_rank):
                                      4: "lean", 5: "cta", 6: "async"}[info["staged"]],
                           "bytes": nb, "avg_us": 1e3 * sum(ts) / len(ts),
                           "GBps": nb / (sum(ts) / len(ts) / 1e3) / 1e9})
-    tot_b = sum(p["bytes"] for p in per_phase) * args.steps
-    tot_ms = sum(lt)
     peak, peak_src = load_peaks()
+    pinfo = plan.persistent()
+    if pinfo["precond"]:
+        # the timed step is ONE persistent launch (both sweeps, all phases)
+        kernel_name = (f"pcg_persistent mode=precond (cooperative, grid {pinfo['grid']} "
+                       f"CTAs, {2 * hl.n_c - 1} in-kernel grid barriers)")
+        tot_b = step_bytes * args.steps
+        tot_ms = dev_ms
+        n_launch = args.steps
+    else:
+        kernel_name = "HBMC sweep, one launch per color phase"
+        tot_b = sum(p["bytes"] for p in per_phase) * args.steps
+        tot_ms = sum(lt)
+        n_launch = len(lt)
     achieved = tot_b / (tot_ms / 1e3) / 1e9
 
     # ---------------- e2e through the public API (host buffers)
@@ -363,17 +374,18 @@ def run_ours(args, rank, world, local_rank):
                        "n_c": hl.n_c, "bytes_per_step": step_bytes,
                        "l2": "flushed before every timed step (256 MiB read)",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
-            "roofline": {"bound": "hbm", "kernel": "HBMC sweep (one launch per color phase)",
+            "roofline": {"bound": "hbm", "kernel": kernel_name,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
-                         "launches": len(lt), "avg_launch_us": 1e3 * tot_ms / max(1, len(lt)),
-                         "algorithmic_bytes_per_launch": tot_b / max(1, len(lt)),
-                         "traffic": None, "phases": per_phase},
+                         "launches": n_launch, "avg_launch_us": 1e3 * tot_ms / max(1, n_launch),
+                         "algorithmic_bytes_per_launch": tot_b / max(1, n_launch),
+                         "traffic": args.traffic,
+                         "per_phase_kernels": per_phase},
             "cpu_baseline": cb,
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_pad, "d2h_bytes_per_step": 8 * n_pad,
                     "ms_per_step": e2e_ms_max / args.steps},
-            "gpu_launches": launches,
+            "gpu_launches": args.steps if pinfo["precond"] else launches,
             "clocks": clk.summary(),
             "iccg": {"iterations": int(rep.iterations),
                      "reference_iterations": ref.get("iterations"),
@@ -404,6 +416,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (profiles/)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", 0))

@@ -259,6 +259,10 @@ int tb_plan_sweep_phase(tb_plan *plan, int forward, int64_t phase,
 int tb_plan_phase_info(const tb_plan *plan, int forward, int64_t phase,
                        int32_t *staged, int32_t *warps, int32_t *grid,
                        int32_t *max_slots);
+/* Whether tb_plan_precond / tb_pcg run as one persistent cooperative launch
+ * (all color phases separated by in-kernel grid barriers) and its grid. */
+int tb_plan_persistent(const tb_plan *plan, int32_t *precond, int32_t *pcg,
+                       int32_t *grid);
 /* number of grid-wide phase boundaries one sweep crosses (n_c - 1) */
 int tb_plan_barriers_per_sweep(const tb_plan *plan, int64_t *count);
 

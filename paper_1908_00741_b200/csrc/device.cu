@@ -1446,6 +1446,15 @@ extern "C" int tb_plan_sweep_phase(tb_plan *pl, int forward, int64_t phase,
   return TB_OK;
 }
 
+extern "C" int tb_plan_persistent(const tb_plan *pl, int32_t *precond, int32_t *pcg,
+                                  int32_t *grid) {
+  if (!pl) return fail(TB_EINVAL, "null plan");
+  *precond = pl->persist_ok;
+  *pcg = pl->persist_ok && pl->persist_pcg_ok;
+  *grid = pl->persist_grid;
+  return TB_OK;
+}
+
 extern "C" int tb_plan_phase_info(const tb_plan *pl, int forward, int64_t phase,
                                   int32_t *staged, int32_t *warps, int32_t *grid,
                                   int32_t *max_slots) {

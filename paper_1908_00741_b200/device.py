@@ -288,6 +288,11 @@ class DevicePlan:
         check(LIB.tb_plan_phase_info(self.handle, 1 if forward else 0, int(phase), *vals))
         return dict(zip(("staged", "warps", "grid", "max_slots"), (v.value for v in vals)))
 
+    def persistent(self):
+        vals = [_lib.i32() for _ in range(3)]
+        check(LIB.tb_plan_persistent(self.handle, *vals))
+        return dict(zip(("precond", "pcg", "grid"), (v.value for v in vals)))
+
     def barriers_per_sweep(self):
         v = _lib.i64()
         check(LIB.tb_plan_barriers_per_sweep(self.handle, v))
