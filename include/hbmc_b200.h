@@ -263,6 +263,9 @@ int tb_plan_phase_info(const tb_plan *plan, int forward, int64_t phase,
  * (all color phases separated by in-kernel grid barriers) and its grid. */
 int tb_plan_persistent(const tb_plan *plan, int32_t *precond, int32_t *pcg,
                        int32_t *grid);
+/* Phase timestamps (%globaltimer, ns) of one steady PCG iteration of the
+ * persistent kernel; the plan must be created with TB_TRACE=1 (diagnostics). */
+int tb_plan_trace(const tb_plan *plan, uint64_t *out64 /* [64] */);
 /* number of grid-wide phase boundaries one sweep crosses (n_c - 1) */
 int tb_plan_barriers_per_sweep(const tb_plan *plan, int64_t *count);
 

@@ -99,6 +99,7 @@ _SIGS = {
     "tb_plan_spmv": [vp, vp, vp, vp],
     "tb_plan_barriers_per_sweep": [vp, P_i64],
     "tb_plan_sweep_phase": [vp, C.c_int, i64, vp, vp, vp],
+    "tb_plan_trace": [vp, vp],
     "tb_plan_persistent": [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
     "tb_plan_phase_info": [vp, C.c_int, i64, C.POINTER(i32), C.POINTER(i32),
                            C.POINTER(i32), C.POINTER(i32)],

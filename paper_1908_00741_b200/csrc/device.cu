@@ -23,6 +23,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -301,18 +302,35 @@ __global__ void __launch_bounds__(kBlock)
 
 // Grid-stride loops below process 4 strided elements per trip with all their
 // loads issued together (fixed order => deterministic partial sums).
-#define TB_GRID_STRIDE4(BODY)                                                  \
+#define TB_GRID_STRIDE4(...)                                                   \
   {                                                                            \
     const long long stride = (long long)gridDim.x * blockDim.x;               \
     long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;          \
     for (; i0 + 3 * stride < n; i0 += 4 * stride) {                           \
       _Pragma("unroll") for (int u = 0; u < 4; ++u) {                          \
         const long long i = i0 + u * stride;                                   \
-        BODY                                                                   \
+        __VA_ARGS__                                                            \
       }                                                                        \
     }                                                                          \
     for (long long i = i0; i < n; i += stride) {                               \
-      BODY                                                                     \
+      __VA_ARGS__                                                              \
+    }                                                                          \
+  }
+
+// Same over element PAIRS (16-byte accesses), i = first index of the pair;
+// requires n even.
+#define TB_PAIRS4(...)                                                         \
+  {                                                                            \
+    const long long stride = 2LL * gridDim.x * blockDim.x;                    \
+    long long i0 = 2LL * ((long long)blockIdx.x * blockDim.x + threadIdx.x);  \
+    for (; i0 + 3 * stride < n; i0 += 4 * stride) {                           \
+      _Pragma("unroll") for (int u = 0; u < 4; ++u) {                          \
+        const long long i = i0 + u * stride;                                   \
+        __VA_ARGS__                                                            \
+      }                                                                        \
+    }                                                                          \
+    for (long long i = i0; i < n; i += stride) {                               \
+      __VA_ARGS__                                                              \
     }                                                                          \
   }
 
@@ -382,8 +400,12 @@ __global__ void __launch_bounds__(kBlock)
 // ------------------------------------------------------------ persistent
 // Whole preconditioner application (mode 0) or whole PCG solve (mode 1) in
 // one cooperative launch; see persist.cuh.  Writes the final PcgState.
-template <int KC>
-__global__ void __launch_bounds__(persist::kThreads, 2) pcg_persistent(persist::Params P) {
+// __grid_constant__: device functions take `const Params &`; without it the
+// parameter block would be copied to local memory and every field access
+// would become a local load.
+template <int KC, bool FLOW>
+__global__ void __launch_bounds__(persist::kThreads, 2)
+    pcg_persistent(const __grid_constant__ persist::Params P) {
   extern __shared__ __align__(16) double psm[];
   const int T = blockDim.x, b_s = P.b_s;
   double *ys = psm;
@@ -394,9 +416,21 @@ __global__ void __launch_bounds__(persist::kThreads, 2) pcg_persistent(persist::
   const int gthreads = gridDim.x * blockDim.x;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = P.n;
+  // z = M src; returns this thread's partial of dotv . z (dotv may be null).
+  // Dataflow path: both sweeps with per-block flags and no grid barrier;
+  // the caller's next grid_sum / grid_sync orders z before its readers.
+  auto precond = [&](const double *src, double *dst, unsigned epoch, const double *dotv) {
+    if constexpr (FLOW)
+      return persist::sweep_pair_dataflow<KC>(P, src, P.y, dst, epoch, dotv, ys, offs, lens);
+    persist::sweep<true, KC>(P, src, P.y, ys, offs, lens);
+    persist::sweep<false, KC>(P, P.y, dst, ys, offs, lens);
+    double d = 0.0;
+    if (dotv)
+      for (int i = gtid; i < n; i += gthreads) d += __ldcg(dotv + i) * __ldcg(dst + i);
+    return d;
+  };
   if (P.mode == 0) {
-    persist::sweep<true, KC>(P, P.pre_src, P.y, ys, offs, lens);
-    persist::sweep<false, KC>(P, P.y, P.pre_dst, ys, offs, lens);
+    precond(P.pre_src, P.pre_dst, P.epoch, nullptr);
     return;
   }
   const double tol = st->tol;
@@ -422,20 +456,16 @@ __global__ void __launch_bounds__(persist::kThreads, 2) pcg_persistent(persist::
     return;
   }
   if (gtid == 0) P.hist[0] = 1.0;
-  persist::sweep<true, KC>(P, P.r, P.y, ys, offs, lens);
-  persist::sweep<false, KC>(P, P.y, P.z, ys, offs, lens);
-  part = 0.0;
-  for (int i = gtid; i < n; i += gthreads) {
-    const double zi = __ldcg(P.z + i);
-    part += __ldcg(P.r + i) * zi;
-    P.p[i] = zi;
-  }
-  double rz = persist::grid_sum(P, part, 1, sh);
+  double rz = persist::grid_sum(P, precond(P.r, P.z, P.epoch, P.r), 1, sh);
+  for (int i = gtid; i < n; i += gthreads) P.p[i] = __ldcg(P.z + i);
+  persist::grid_sync(P);
   long long j = 1, iters = 0;
   int converged = 0, status = TB_OK;
   double bd_val = 0.0, rel = 1.0;
   for (; j <= max_iters; ++j) {
+    if (j == 3) persist::stamp(P, 0);
     const double pap = persist::grid_sum(P, persist::spmv_dot(P), 2, sh);
+    if (j == 3) persist::stamp(P, 1);
     if (pap <= 0.0) {  // src/solver.py:176-177
       status = TB_ECG_BREAKDOWN;
       bd_val = pap;
@@ -443,13 +473,22 @@ __global__ void __launch_bounds__(persist::kThreads, 2) pcg_persistent(persist::
     }
     const double alpha = rz / pap;
     part = 0.0;
-    for (int i = gtid; i < n; i += gthreads) {
-      P.x[i] = __dadd_rn(P.x[i], __dmul_rn(alpha, __ldcg(P.p + i)));
-      const double ri = __dsub_rn(P.r[i], __dmul_rn(alpha, __ldcg(P.ap + i)));
-      P.r[i] = ri;
-      part += ri * ri;
-    }
+    // 16-byte accesses, 4 pairs per trip (n is even: a multiple of b_s*w)
+    TB_PAIRS4({
+      const double2 xo = *(const double2 *)(P.x + i), po = __ldcg((const double2 *)(P.p + i));
+      const double2 ro = *(const double2 *)(P.r + i), ao = __ldcg((const double2 *)(P.ap + i));
+      double2 xn, rn;
+      xn.x = __dadd_rn(xo.x, __dmul_rn(alpha, po.x));
+      xn.y = __dadd_rn(xo.y, __dmul_rn(alpha, po.y));
+      rn.x = __dsub_rn(ro.x, __dmul_rn(alpha, ao.x));
+      rn.y = __dsub_rn(ro.y, __dmul_rn(alpha, ao.y));
+      *(double2 *)(P.x + i) = xn;
+      *(double2 *)(P.r + i) = rn;
+      part += rn.x * rn.x;
+      part += rn.y * rn.y;
+    })
     rel = sqrt(persist::grid_sum(P, part, 3, sh)) / bnorm;
+    if (j == 3) persist::stamp(P, 2);
     if (gtid == 0) P.hist[j] = rel;
     iters = j;
     if (rel < tol) {
@@ -457,16 +496,21 @@ __global__ void __launch_bounds__(persist::kThreads, 2) pcg_persistent(persist::
       break;
     }
     if (j == max_iters) break;
-    persist::sweep<true, KC>(P, P.r, P.y, ys, offs, lens);
-    persist::sweep<false, KC>(P, P.y, P.z, ys, offs, lens);
-    part = 0.0;
-    for (int i = gtid; i < n; i += gthreads) part += __ldcg(P.r + i) * __ldcg(P.z + i);
-    const double rzn = persist::grid_sum(P, part, 1, sh);
+    const double rzn =
+        persist::grid_sum(P, precond(P.r, P.z, P.epoch + (unsigned)j, P.r), 1, sh);
+    if (j == 3) persist::stamp(P, 3);
     const double beta = rzn / rz;
     rz = rzn;
-    for (int i = gtid; i < n; i += gthreads)
-      P.p[i] = __dadd_rn(__ldcg(P.z + i), __dmul_rn(beta, __ldcg(P.p + i)));
+    TB_PAIRS4({
+      const double2 zo = __ldcg((const double2 *)(P.z + i));
+      const double2 po = *(const double2 *)(P.p + i);
+      double2 pn;
+      pn.x = __dadd_rn(zo.x, __dmul_rn(beta, po.x));
+      pn.y = __dadd_rn(zo.y, __dmul_rn(beta, po.y));
+      *(double2 *)(P.p + i) = pn;
+    })
     persist::grid_sync(P);
+    if (j == 3) persist::stamp(P, 4);
   }
   if (gtid == 0) {
     st->bnorm = bnorm;
@@ -668,6 +712,13 @@ struct tb_plan {
   int *color_lvl1_dev = nullptr;
   unsigned *bar = nullptr;  // [count, generation]
   double *ppartials = nullptr;
+  // dataflow sweeps: per level-1 block dependency lists + completion flags
+  long long n_lvl1_flow = 0;  // 0 = barrier-separated color phases
+  int *fdep_ptr = nullptr, *fdep = nullptr, *bdep_ptr = nullptr, *bdep = nullptr;
+  unsigned *flags = nullptr;  // [2 * n_lvl1]: forward, backward
+  unsigned char *small = nullptr;  // per level-1 block: short-chain bits
+  unsigned long long *trace = nullptr;  // TB_TRACE=1: in-kernel phase stamps
+  unsigned epoch = 1;
 };
 
 namespace {
@@ -1154,12 +1205,12 @@ int build_graph(tb_plan *pl, const double *b, double *x) {
 // ------------------------------------------------------------ persistent host side
 using PersistFn = void (*)(persist::Params);
 
-PersistFn persist_fn(int kc) {
+PersistFn persist_fn(int kc, bool flow) {
   switch (kc) {
-    case 2: return pcg_persistent<2>;
-    case 4: return pcg_persistent<4>;
-    case 6: return pcg_persistent<6>;
-    default: return pcg_persistent<8>;
+    case 2: return flow ? pcg_persistent<2, true> : pcg_persistent<2, false>;
+    case 4: return flow ? pcg_persistent<4, true> : pcg_persistent<4, false>;
+    case 6: return flow ? pcg_persistent<6, true> : pcg_persistent<6, false>;
+    default: return flow ? pcg_persistent<8, true> : pcg_persistent<8, false>;
   }
 }
 
@@ -1186,10 +1237,14 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   int v = 0;
   CU(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
   if (smem > (size_t)v) return TB_OK;
-  PersistFn fn = persist_fn(kc);
-  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)T, smem));
+  int per_sm = 1 << 30;
+  for (bool flow : {false, true}) {  // the grid must be co-resident for either variant
+    PersistFn fn = persist_fn(kc, flow);
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int ps = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, (int)T, smem));
+    per_sm = ps < per_sm ? ps : per_sm;
+  }
   if (per_sm < 1) return TB_OK;
   if (per_sm > 2) per_sm = 2;
   pl->persist_kc = kc;
@@ -1202,15 +1257,91 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   CU(cudaMemset(pl->bar, 0, 2 * sizeof(unsigned)));
   CU(cudaMalloc((void **)&pl->ppartials, sizeof(double) * persist::kSlots * pl->persist_grid));
   pl->persist_ok = true;
+  // ---- dataflow sweeps (w == 32): level-1 block dependency lists.  Every
+  // cross-block column of a forward row must lie in an EARLIER level-1
+  // block and of a backward row in a LATER one (HBMC structure); otherwise
+  // keep the barrier-separated phases.
+  const char *df = getenv("TB_DATAFLOW");
+  if (pl->w == 32 && !(df && !strcmp(df, "0"))) {
+    const long long nl = pl->color_lvl1.back();
+    const long long span = pl->b_s * 32;
+    std::vector<int> fp, fd, bp, bd, tmp;
+    std::vector<unsigned char> small(nl, 0);
+    bool ok = true;
+    auto build = [&](const tb_sell_host &M, std::vector<int> &ptr, std::vector<int> &dep,
+                     bool fwd) {
+      ptr.assign(nl + 1, 0);
+      dep.clear();
+      for (long long k = 0; k < nl && ok; ++k) {
+        tmp.clear();
+        int maxlen = 0;
+        for (long long sid = k * pl->b_s; sid < (k + 1) * pl->b_s; ++sid)
+          maxlen = M.slice_len[sid] > maxlen ? M.slice_len[sid] : maxlen;
+        if (maxlen <= 2) small[k] |= fwd ? 1 : 2;
+        for (long long sid = k * pl->b_s; sid < (k + 1) * pl->b_s; ++sid) {
+          const long long off = M.slice_ptr[sid], cnt = (long long)M.slice_len[sid] * 32;
+          for (long long q = off; q < off + cnt; ++q) {
+            const long long kb = M.col_idx[q] / span;
+            if (kb == k) continue;
+            if (fwd ? kb > k : kb < k) ok = false;
+            tmp.push_back((int)kb);
+          }
+        }
+        std::sort(tmp.begin(), tmp.end());
+        tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+        dep.insert(dep.end(), tmp.begin(), tmp.end());
+        ptr[k + 1] = (int)dep.size();
+      }
+    };
+    build(d->L_sell, fp, fd, true);
+    build(d->U_sell, bp, bd, false);
+    if (ok && nl > 0) {
+      if (fd.empty()) fd.push_back(0);
+      if (bd.empty()) bd.push_back(0);
+      if ((rc = upload(&pl->fdep_ptr, fp.data(), (long long)fp.size()))) return rc;
+      if ((rc = upload(&pl->fdep, fd.data(), (long long)fd.size()))) return rc;
+      if ((rc = upload(&pl->bdep_ptr, bp.data(), (long long)bp.size()))) return rc;
+      if ((rc = upload(&pl->bdep, bd.data(), (long long)bd.size()))) return rc;
+      if ((rc = upload(&pl->small, small.data(), nl))) return rc;
+      CU(cudaMalloc((void **)&pl->flags, sizeof(unsigned) * 2 * nl));
+      CU(cudaMemset(pl->flags, 0, sizeof(unsigned) * 2 * nl));
+      pl->n_lvl1_flow = nl;
+      pl->epoch = 1;
+    }
+  }
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
+  if (env_int("TB_TRACE", 0)) {
+    CU(cudaMalloc((void **)&pl->trace, 64 * sizeof(unsigned long long)));
+    CU(cudaMemset(pl->trace, 0, 64 * sizeof(unsigned long long)));
+  }
   return TB_OK;
 }
 
 // mode 0: z = M r (src -> dst); mode 1: whole PCG (b, x; state preset).
+// `applications` = preconditioner applications the launch may perform (epochs).
 int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, const double *b,
-                      double *x, cudaStream_t s) {
+                      double *x, cudaStream_t s, long long applications = 1) {
   persist::Params P;
   memset(&P, 0, sizeof(P));
+  if (pl->n_lvl1_flow > 0) {
+    if ((unsigned long long)pl->epoch + (unsigned long long)applications + 2 > 0xF0000000ull) {
+      CU(cudaMemsetAsync(pl->flags, 0, sizeof(unsigned) * 2 * pl->n_lvl1_flow, s));
+      pl->epoch = 1;
+    }
+    P.n_lvl1 = (int)pl->n_lvl1_flow;
+    P.fdep_ptr = pl->fdep_ptr;
+    P.fdep = pl->fdep;
+    P.bdep_ptr = pl->bdep_ptr;
+    P.bdep = pl->bdep;
+    P.fflag = pl->flags;
+    P.bflag = pl->flags + pl->n_lvl1_flow;
+    P.small = pl->small;
+  }
+  P.trace = pl->trace;
+  {
+    P.epoch = pl->epoch;
+    pl->epoch += (unsigned)(applications + 1);
+  }
   P.mode = mode;
   P.n = (int)pl->n;
   P.w = (int)pl->w;
@@ -1247,7 +1378,7 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.state = pl->st;
   P.watchdog = 4000000000LL;  // ~2 s at 1.9 GHz per barrier wait
   void *args[] = {&P};
-  CU(cudaLaunchCooperativeKernel((const void *)persist_fn(pl->persist_kc),
+  CU(cudaLaunchCooperativeKernel((const void *)persist_fn(pl->persist_kc, P.n_lvl1 > 0),
                                  dim3(pl->persist_grid), dim3(persist::kThreads), args,
                                  pl->persist_smem, s));
   return TB_OK;
@@ -1377,6 +1508,12 @@ extern "C" int tb_plan_destroy(tb_plan *pl) {
   cudaFree(pl->color_lvl1_dev);
   cudaFree(pl->bar);
   cudaFree(pl->ppartials);
+  cudaFree(pl->fdep_ptr);
+  cudaFree(pl->fdep);
+  cudaFree(pl->bdep_ptr);
+  cudaFree(pl->bdep);
+  cudaFree(pl->flags);
+  cudaFree(pl->small);
   if (pl->ev_in) cudaEventDestroy(pl->ev_in);
   if (pl->ev_out) cudaEventDestroy(pl->ev_out);
   if (pl->stream) cudaStreamDestroy(pl->stream);
@@ -1446,6 +1583,13 @@ extern "C" int tb_plan_sweep_phase(tb_plan *pl, int forward, int64_t phase,
   return TB_OK;
 }
 
+extern "C" int tb_plan_trace(const tb_plan *pl, uint64_t *out64) {
+  if (!pl) return fail(TB_EINVAL, "null plan");
+  if (!pl->trace) return fail(TB_EINVAL, "plan created without TB_TRACE=1");
+  CU(cudaMemcpy(out64, pl->trace, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return TB_OK;
+}
+
 extern "C" int tb_plan_persistent(const tb_plan *pl, int32_t *precond, int32_t *pcg,
                                   int32_t *grid) {
   if (!pl) return fail(TB_EINVAL, "null plan");
@@ -1512,7 +1656,8 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
   const bool persistent = check_every <= 0 && pl->persist_ok && pl->persist_pcg_ok;
   if (persistent) {
     if ((rc = sync_in(pl, stream))) return rc;
-    if ((rc = launch_persistent(pl, 1, nullptr, nullptr, b, x, pl->stream))) return rc;
+    if ((rc = launch_persistent(pl, 1, nullptr, nullptr, b, x, pl->stream, max_iters + 1)))
+      return rc;
     CU(cudaMemcpyAsync(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost, pl->stream));
     CU(cudaStreamSynchronize(pl->stream));
   } else if (check_every > 0) {

@@ -46,6 +46,8 @@ __device__ __forceinline__ double ldv(const double *p) {
 
 // One lane's b_s-step walk.  W > 0: compile-time slice width; W == 0: w_rt.
 // Shared memory: ys/offs/lens columns of this thread ([b_s][nt] each).
+// dotv != nullptr: also accumulate dotv[row] * result into *dotacc (r . z
+// fused into the backward sweep), rows in walk order.
 template <bool FWD, int KC, int W, bool CG>
 __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_ptr,
                                            const int *__restrict__ slice_len,
@@ -53,7 +55,9 @@ __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_p
                                            const double *__restrict__ val,
                                            const double *__restrict__ inv_d,
                                            const double *src, double *dst, int w_rt, int b_s,
-                                           int k, int j, double *ys, int *offs, int *lens) {
+                                           int k, int j, double *ys, int *offs, int *lens,
+                                           const double *dotv = nullptr,
+                                           double *dotacc = nullptr) {
   const int w = W > 0 ? W : w_rt;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int span = b_s * w;
@@ -120,6 +124,7 @@ __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_p
     y = __dmul_rn(y, b.idg);
     ys[i * nt + tid] = y;
     dst[row] = y;
+    if (dotv) *dotacc += ldv<CG>(dotv + row) * y;
   };
 
   Buf<KC> A, B;
