@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kBlock)
 // ------------------------------------------------------------ SpMV
 // K/numba_backend.py:26-37: out = 0; out += v * x[col] per slot in stored
 // order.  Optional fused epilogue: pap = p . (A p) and alpha = rz / pap.
-template <bool DOT>
+template <bool DOT, bool PAIRED = false>
 __global__ void __launch_bounds__(kBlock)
     spmv_sell(long long n, const long long *__restrict__ slice_ptr,
               const int *__restrict__ slice_len, const int *__restrict__ col,
@@ -199,6 +199,14 @@ __global__ void __launch_bounds__(kBlock)
   constexpr int CH = 8;  // slots whose loads / gathers are in flight together
   for (long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x; row < n;
        row += (long long)gridDim.x * blockDim.x) {
+    if (PAIRED) {
+      const long long s = row / w;
+      const double acc = persist::sell_row_paired<4>(val, col, (int)slice_ptr[s], slice_len[s],
+                                                     w, (int)(row - s * w), x);
+      out[row] = acc;
+      if (DOT) part += __ldcg(x + row) * acc;
+      continue;
+    }
     const long long s = row / w;
     const int j = (int)(row - s * w);
     const long long off = slice_ptr[s] + j;
@@ -464,7 +472,8 @@ __global__ void __launch_bounds__(persist::kThreads, 2)
   double bd_val = 0.0, rel = 1.0;
   for (; j <= max_iters; ++j) {
     if (j == 3) persist::stamp(P, 0);
-    const double pap = persist::grid_sum(P, persist::spmv_dot(P), 2, sh);
+    const double pap = persist::grid_sum(
+        P, P.a_paired ? persist::spmv_dot_paired(P) : persist::spmv_dot(P), 2, sh);
     if (j == 3) persist::stamp(P, 1);
     if (pap <= 0.0) {  // src/solver.py:176-177
       status = TB_ECG_BREAKDOWN;
@@ -554,6 +563,7 @@ struct DevSell {
   long long *slice_ptr = nullptr;
   int *slice_len = nullptr, *col = nullptr;
   double *val = nullptr;
+  bool paired = false;  // slots stored in the paired layout (upload_sell_paired)
 };
 
 struct DevCsr {
@@ -616,6 +626,37 @@ int upload_sell_step_major(DevSell &d, const tb_sell_host &h,
   if (pos != d.slots) return fail(TB_EINVAL, "step-major upload: slice lengths inconsistent");
   int rc;
   if ((rc = upload(&d.slice_ptr, sp.data(), h.n_slices + 1))) return rc;
+  if ((rc = upload(&d.slice_len, h.slice_len, h.n_slices))) return rc;
+  if ((rc = upload(&d.col, col.data(), d.slots))) return rc;
+  if ((rc = upload(&d.val, val.data(), d.slots))) return rc;
+  return TB_OK;
+}
+
+// Upload a SELL matrix in the PAIRED device layout (persist.cuh:
+// sell_row_paired): inside each slice, slots 2p, 2p+1 of lane j at
+// off + p*2w + 2j, an odd last slot in a tail row at off + (len/2)*2w + j.
+// Same slice offsets and sizes; only the order of slots inside a slice.
+int upload_sell_paired(DevSell &d, const tb_sell_host &h) {
+  d.n_slices = h.n_slices;
+  d.width = h.width;
+  d.slots = h.n_slices > 0 ? h.slice_ptr[h.n_slices] : 0;
+  d.paired = true;
+  const long long w = h.width;
+  std::vector<int> col(d.slots);
+  std::vector<double> val(d.slots);
+  for (long long s = 0; s < h.n_slices; ++s) {
+    const long long off = h.slice_ptr[s], len = h.slice_len[s], np = len / 2;
+    for (long long t = 0; t < len; ++t)
+      for (long long j = 0; j < w; ++j) {
+        const long long src = off + t * w + j;
+        const long long dst = t < 2 * np ? off + (t / 2) * 2 * w + 2 * j + (t & 1)
+                                         : off + np * 2 * w + j;
+        col[dst] = h.col_idx[src];
+        val[dst] = h.vals[src];
+      }
+  }
+  int rc;
+  if ((rc = upload(&d.slice_ptr, (const long long *)h.slice_ptr, h.n_slices + 1))) return rc;
   if ((rc = upload(&d.slice_len, h.slice_len, h.n_slices))) return rc;
   if ((rc = upload(&d.col, col.data(), d.slots))) return rc;
   if ((rc = upload(&d.val, val.data(), d.slots))) return rc;
@@ -1081,13 +1122,15 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
     return fail(TB_EINVAL, "plan has no matrix A (preconditioner-only plan)");
   if (pl->spmv_format == TB_SPMV_SELL) {
     if (dot)
-      spmv_sell<true><<<reduce_grid(n, 1), kBlock, 0, s>>>(
-          n, pl->A.slice_ptr, pl->A.slice_len, pl->A.col, pl->A.val,
-          (int)pl->A.width, x, out, pl->partials, pl->st);
+      (pl->A.paired ? spmv_sell<true, true> : spmv_sell<true, false>)
+          <<<reduce_grid(n, 1), kBlock, 0, s>>>(n, pl->A.slice_ptr, pl->A.slice_len,
+                                                pl->A.col, pl->A.val, (int)pl->A.width, x,
+                                                out, pl->partials, pl->st);
     else
-      spmv_sell<false><<<grid_for(n), kBlock, 0, s>>>(
-          n, pl->A.slice_ptr, pl->A.slice_len, pl->A.col, pl->A.val,
-          (int)pl->A.width, x, out, nullptr, nullptr);
+      (pl->A.paired ? spmv_sell<false, true> : spmv_sell<false, false>)
+          <<<grid_for(n), kBlock, 0, s>>>(n, pl->A.slice_ptr, pl->A.slice_len, pl->A.col,
+                                          pl->A.val, (int)pl->A.width, x, out, nullptr,
+                                          nullptr);
   } else {
     if (dot)
       spmv_csr<true><<<reduce_grid(n), kBlock, 0, s>>>(
@@ -1362,6 +1405,7 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.Acol = pl->A.col;
   P.Aval = pl->A.val;
   P.aw = (int)(pl->A.width > 0 ? pl->A.width : 1);
+  P.a_paired = pl->A.paired ? 1 : 0;
   P.b = b;
   P.x = x;
   P.r = pl->r;
@@ -1457,7 +1501,10 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
   } else if (d->spmv_format == TB_SPMV_SELL) {
     if (d->A_sell.n_slices * d->A_sell.width < d->n)
       return bail(fail(TB_EINVAL, "plan_create: SELL A smaller than n"));
-    if ((rc = upload_sell(pl->A, d->A_sell))) return bail(rc);
+    const bool pair_a = env_int("TB_APAIR", 0) != 0 && d->A_sell.width % 2 == 0 &&
+                        d->A_sell.slice_ptr[d->A_sell.n_slices] <= 0x7fffffffLL;
+    if ((rc = pair_a ? upload_sell_paired(pl->A, d->A_sell) : upload_sell(pl->A, d->A_sell)))
+      return bail(rc);
   } else {
     if ((rc = upload_csr(pl->Ac, d->A_csr))) return bail(rc);
   }

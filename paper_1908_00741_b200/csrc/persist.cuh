@@ -44,6 +44,7 @@ struct Params {
   const int *Asl, *Acol;
   const double *Aval;
   int aw;
+  int a_paired;           // A stored in the paired layout
   // vectors
   const double *b;
   double *x, *r, *y, *z, *p, *ap;
@@ -258,6 +259,77 @@ __device__ __forceinline__ double sweep_pair_dataflow(const Params &P, const dou
 }
 
 // ---------------------------------------------------------------- SpMV
+// Paired SELL (device layout of A, see device.cu:pair_sell): inside a slice
+// of width w and length len, slots 2p and 2p+1 of lane j are adjacent at
+// off + p*2w + 2j (one 16-byte value load, one 8-byte column load); an odd
+// last slot sits in a tail row at off + (len/2)*2w + j.  Same bytes, same
+// slot order, half the load instructions.
+// acc = 0; acc = acc + v*x over the row's slots in order (K/numba_backend.py:26-37).
+template <int MAXP>
+__device__ __forceinline__ double sell_row_paired(const double *__restrict__ vals,
+                                                  const int *__restrict__ cols, int off, int len,
+                                                  int w, int j, const double *x) {
+  double acc = 0.0;
+  const int np = len >> 1;
+  for (int p0 = 0; p0 < np; p0 += MAXP) {
+    double2 v[MAXP];
+    int2 c[MAXP];
+    double x0[MAXP], x1[MAXP];
+#pragma unroll
+    for (int u = 0; u < MAXP; ++u) {
+      const bool in = p0 + u < np;
+      const int o = off + (p0 + u) * 2 * w + 2 * j;
+      v[u] = in ? __ldg((const double2 *)(vals + o)) : make_double2(0.0, 0.0);
+      c[u] = in ? __ldg((const int2 *)(cols + o)) : make_int2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < MAXP; ++u) {
+      const bool in = p0 + u < np;
+      x0[u] = in ? __ldcg(x + c[u].x) : 0.0;
+      x1[u] = in ? __ldcg(x + c[u].y) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < MAXP; ++u)
+      if (p0 + u < np) {
+        acc = __dadd_rn(acc, __dmul_rn(v[u].x, x0[u]));
+        acc = __dadd_rn(acc, __dmul_rn(v[u].y, x1[u]));
+      }
+  }
+  if (len & 1) {
+    const int o = off + np * 2 * w + j;
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(vals + o), __ldcg(x + __ldg(cols + o))));
+  }
+  return acc;
+}
+
+// Paired-layout SpMV with the p.Ap partial; two rows per trip (i, i+stride).
+__device__ __forceinline__ double spmv_dot_paired(const Params &P) {
+  const int gthreads = gridDim.x * blockDim.x;
+  double part = 0.0;
+  int row = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; row + gthreads < P.n; row += 2 * gthreads) {
+    const int r1 = row + gthreads;
+    const int s0 = row / P.aw, s1 = r1 / P.aw;
+    const int off0 = (int)P.Asp[s0], off1 = (int)P.Asp[s1];
+    const int len0 = P.Asl[s0], len1 = P.Asl[s1];
+    const double p0 = ldcg(P.p + row), p1 = ldcg(P.p + r1);
+    const double a0 = sell_row_paired<4>(P.Aval, P.Acol, off0, len0, P.aw, row - s0 * P.aw, P.p);
+    const double a1 = sell_row_paired<4>(P.Aval, P.Acol, off1, len1, P.aw, r1 - s1 * P.aw, P.p);
+    P.ap[row] = a0;
+    P.ap[r1] = a1;
+    part += p0 * a0;
+    part += p1 * a1;
+  }
+  for (; row < P.n; row += gthreads) {
+    const int s = row / P.aw;
+    const double a = sell_row_paired<4>(P.Aval, P.Acol, (int)P.Asp[s], P.Asl[s], P.aw,
+                                        row - s * P.aw, P.p);
+    P.ap[row] = a;
+    part += ldcg(P.p + row) * a;
+  }
+  return part;
+}
+
 // ap = A p (K/numba_backend.py:26-37); returns this thread's p.ap partial.
 // Two rows per trip (rows i and i + stride) so two rows' loads and gathers
 // are in flight together; 8 slots per chunk.  Row order of the partial sum
