@@ -234,7 +234,15 @@ typedef struct {
     /* SpMV */
     tb_sell_host A_sell;
     tb_csr_host A_csr;
+    /* TB_PLAN_* flags (ABI 2) */
+    int64_t flags;
 } tb_plan_desc;
+
+/* The plan is one rank of a row-partitioned system (partition.py): columns
+ * may address halo entries beyond n, and the sweeps run phase by phase
+ * (tb_plan_sweep_phase) with halo exchanges in between -- no persistent /
+ * dataflow kernel is configured. */
+#define TB_PLAN_PARTITIONED 1
 
 typedef struct tb_plan tb_plan;
 
@@ -287,6 +295,28 @@ typedef struct {
 int tb_pcg(tb_plan *plan, const double *b, double *x, double tol,
            int64_t max_iters, int64_t check_every, void *stream,
            tb_pcg_report *report, double *history_host);
+
+/* =========================================================================
+ * Row-partitioned ICCG (csrc/dist.cu).  Device pointers; the
+ * scalar slots s[] live in device memory and are all-reduced across ranks
+ * by the caller (NCCL) between these calls.
+ * ========================================================================= */
+
+/* dst[i] = src[idx[i]], i < n: pack one halo exchange step's send buffer. */
+int tb_dev_gather(int64_t n, const int32_t *idx, const double *src, double *dst,
+                  void *stream);
+/* s[slot] = <u, v> over [0, n) (deterministic two-pass; ws >= 1184 doubles).
+ * The rank-local part of the dots of src/solver.py:150-153. */
+int tb_dev_dot(int64_t n, const double *u, const double *v, double *s, int32_t slot,
+               double *ws, void *stream);
+/* alpha = s[num] / s[den]; x += alpha p; r -= alpha ap; s[rr] = <r, r>
+ * (src/solver.py:178-186, rank-local part). */
+int tb_dev_cg_xr(int64_t n, double *s, int32_t num, int32_t den, const double *p,
+                 const double *ap, double *x, double *r, int32_t rr_slot, double *ws,
+                 void *stream);
+/* beta = s[num] / s[den]; p = z + beta p (src/solver.py:190-193). */
+int tb_dev_cg_p(int64_t n, const double *s, int32_t num, int32_t den, const double *z,
+                double *p, void *stream);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,8 @@ TB_SPMV_SELL = 0
 TB_SPMV_CSR = 1
 TB_SPMV_NONE = 2
 
-ABI_VERSION = 1
+ABI_VERSION = 2
+TB_PLAN_PARTITIONED = 1
 
 i64 = C.c_int64
 i32 = C.c_int32
@@ -58,7 +59,7 @@ class TbPlanDesc(C.Structure):
                 ("L_sell", TbSellHost), ("U_sell", TbSellHost),
                 ("L_csr", TbCsrHost), ("U_csr", TbCsrHost),
                 ("fwd_sched", TbSchedHost), ("bwd_sched", TbSchedHost),
-                ("A_sell", TbSellHost), ("A_csr", TbCsrHost)]
+                ("A_sell", TbSellHost), ("A_csr", TbCsrHost), ("flags", i64)]
 
 
 class TbPcgReport(C.Structure):
@@ -104,6 +105,10 @@ _SIGS = {
     "tb_plan_phase_info": [vp, C.c_int, i64, C.POINTER(i32), C.POINTER(i32),
                            C.POINTER(i32), C.POINTER(i32)],
     "tb_pcg": [vp, vp, vp, dbl, i64, i64, vp, C.POINTER(TbPcgReport), vp],
+    "tb_dev_gather": [i64, vp, vp, vp, vp],
+    "tb_dev_dot": [i64, vp, vp, vp, i32, vp, vp],
+    "tb_dev_cg_xr": [i64, vp, i32, i32, vp, vp, vp, vp, i32, vp, vp],
+    "tb_dev_cg_p": [i64, vp, i32, i32, vp, vp, vp],
 }
 
 EXPORTED = sorted(_SIGS) + ["tb_last_error"]

@@ -1487,7 +1487,8 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
     }
     if ((rc = configure_sweeps(pl, d->L_sell, pl->cl_fwd))) return bail(rc);
     if ((rc = configure_sweeps(pl, d->U_sell, pl->cl_bwd))) return bail(rc);
-    if ((rc = configure_persistent(pl, d))) return bail(rc);
+    if (!(d->flags & TB_PLAN_PARTITIONED) && (rc = configure_persistent(pl, d)))
+      return bail(rc);
   } else if (d->precond_kind == TB_PRECOND_TASKS) {
     if ((rc = upload_csr(pl->Lc, d->L_csr))) return bail(rc);
     if ((rc = upload_csr(pl->Uc, d->U_csr))) return bail(rc);

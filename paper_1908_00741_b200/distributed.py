@@ -1,0 +1,358 @@
+"""Row-partitioned HBMC ICCG across ranks.
+
+Each rank owns chunk g of every color's level-1 range (`partition.py`) and
+runs the single-device sweep / SpMV kernels on its local HBMC system.  Per
+preconditioner application there are `n_c - 1` halo exchanges per sweep --
+one after every color phase that a later phase of the same sweep depends on
+(the reference's `n_c - 1` fork-join barriers, `src/precond.py:389-391`) --
+and one p-halo exchange before each SpMV.  CG dot products are reduced
+across ranks (NCCL all-reduce on the device scalars); the only host read per
+iteration is ‖r‖ for the convergence test, as in `src/solver.py:181-187`.
+
+The iteration is `src/solver.py:139-204` restated over partitioned vectors:
+
+    x0 = 0, r = b, z = M r, p = z, rz = <r, z>
+    loop: ap = A p; pap = <p, ap> (<= 0: CgBreakdownError); alpha = rz/pap
+          x += alpha p; r -= alpha ap; rel = ||r||/||b||; stop if rel < tol
+          z = M r; beta = <r, z>/rz; p = z + beta p
+
+Local-rank lockstep: one process may drive several ranks ("virtual ranks",
+e.g. G partitions on one GPU for parity tests, all work serialised on one
+stream -- no rank ever waits on another inside a kernel); with
+torch.distributed initialised, each process drives exactly one rank and
+messages to other processes go through `batch_isend_irecv` (NCCL over
+NVLink on B200s, gloo in the CPU tests).  Every exchange step receives
+directly into the halo slice of the destination vector (the partition
+orders the halo so each message is contiguous); sends are packed by one
+gather kernel per exchange step.
+
+`ops` is the per-rank compute backend.  The product backend is
+`CudaRankOps` (kernels of libhbmc_b200.so through the C ABI); the CPU tests
+plug in an oracle-backed backend to check the exchange logic under gloo.
+"""
+
+import math
+import time
+
+import numpy as np
+
+from . import _lib
+from .partition import partition_hbmc
+
+# device scalar slots
+BB, PAP, RR, RZ0, RZ1 = 0, 1, 2, 3, 4
+N_SCAL = 8
+
+
+class CudaRankOps:
+    """Per-rank device backend: a tb_plan over the local HBMC system plus the
+    distributed-CG vector kernels (`csrc/dist.cu`)."""
+
+    def __init__(self, part, device=None, stream=None):
+        from . import device as D
+        t = D.require_cuda()
+        self.t = t
+        self.part = part
+        self.n = part.n_loc
+        self.ws = t.empty(4096, dtype=t.float64, device="cuda")
+        self.idx = {}
+        self.plan = None
+        if part.n_loc == 0:   # a rank with no level-1 block (tiny systems)
+            return
+        self.plan = D.DevicePlan(kind=_lib.TB_PRECOND_HBMC, n=part.n_loc, n_real=part.n_loc,
+                                 inv_d=part.inv_d, w=part.w, b_s=part.b_s,
+                                 color_lvl1_ranges=part.color_lvl1_ranges,
+                                 L_sell=part.L, U_sell=part.U,
+                                 spmv_format=_lib.TB_SPMV_SELL, A_sell=part.A,
+                                 device=device, partitioned=True)
+
+    def stream(self):
+        from . import device as D
+        return D.current_stream()
+
+    def vec(self, n=None):
+        return self.t.zeros(self.part.n_ext if n is None else n, dtype=self.t.float64,
+                            device="cuda")
+
+    def scalars(self):
+        return self.t.zeros(N_SCAL, dtype=self.t.float64, device="cuda")
+
+    def from_host(self, a):
+        return self.t.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+    def to_host(self, v, n=None):
+        return v[: self.n if n is None else n].cpu().numpy()
+
+    def sweep_phase(self, forward, c, src, dst):
+        if self.plan is not None:
+            self.plan.sweep_phase(forward, c, src, dst)
+
+    def spmv(self, x, out):
+        if self.plan is not None:
+            self.plan.spmv(x, out)
+
+    def pack(self, key, ex, src, buf):
+        if ex.n_send == 0:
+            return
+        idx = self.idx.get(key)
+        if idx is None:
+            idx = self.idx[key] = self.t.from_numpy(ex.send_idx).cuda()
+        _lib.check(_lib.LIB.tb_dev_gather(ex.n_send, _lib.ptr(idx), _lib.ptr(src),
+                                          _lib.ptr(buf), self.stream()))
+
+    def copy_range(self, dst, doff, src, soff, cnt):
+        dst[doff:doff + cnt].copy_(src[soff:soff + cnt])
+
+    def dot(self, u, v, scal, slot):
+        _lib.check(_lib.LIB.tb_dev_dot(self.n, _lib.ptr(u), _lib.ptr(v), _lib.ptr(scal),
+                                       slot, _lib.ptr(self.ws), self.stream()))
+
+    def update_xr(self, scal, num, den, p, ap, x, r, rr_slot):
+        _lib.check(_lib.LIB.tb_dev_cg_xr(self.n, _lib.ptr(scal), num, den, _lib.ptr(p),
+                                         _lib.ptr(ap), _lib.ptr(x), _lib.ptr(r), rr_slot,
+                                         _lib.ptr(self.ws), self.stream()))
+
+    def update_p(self, scal, num, den, z, p):
+        _lib.check(_lib.LIB.tb_dev_cg_p(self.n, _lib.ptr(scal), num, den, _lib.ptr(z),
+                                        _lib.ptr(p), self.stream()))
+
+    def copy(self, dst, src):
+        dst[: self.n].copy_(src[: self.n])
+
+    def fill_zero(self, v):
+        v.zero_()
+
+    def read(self, scal, slots):
+        h = scal.cpu().numpy()
+        return [float(h[s]) for s in slots]
+
+    def add_scal(self, dst, src, slots):
+        for s in slots:
+            dst[s:s + 1].add_(src[s:s + 1])
+
+    def set_scal(self, dst, src, slots):
+        for s in slots:
+            dst[s:s + 1].copy_(src[s:s + 1])
+
+    def close(self):
+        if self.plan is not None:
+            self.plan.close()
+
+
+class DistHbmc:
+    """Lockstep driver of the local ranks of this process.
+
+    parts: RankParts owned by this process (all G for a single process; one
+    per process under torch.distributed, with part.rank == dist rank).
+    """
+
+    def __init__(self, parts, ops, group=None):
+        self.parts = list(parts)
+        self.ops = list(ops)
+        self.world = self.parts[0].world
+        self.local = {p.rank: i for i, p in enumerate(self.parts)}
+        self.group = group
+        self.dist = None
+        if len(self.parts) < self.world:
+            import torch.distributed as dist
+            if not dist.is_initialized():
+                raise RuntimeError("DistHbmc: remote ranks need torch.distributed")
+            self.dist = dist
+        n_c = self.parts[0].n_c
+        self.n_c = n_c
+        self.sendbuf = {}
+        for key_kind in ("fwd", "bwd", "spmv"):
+            for c in (range(n_c) if key_kind != "spmv" else [-1]):
+                for i, p in enumerate(self.parts):
+                    ex = self._ex(p, key_kind, c)
+                    if ex.n_send:
+                        self.sendbuf[(key_kind, c, i)] = self.ops[i].vec(ex.n_send)
+        self.exchanges = 0
+        self.bytes_sent = 0
+
+    @staticmethod
+    def _ex(p, kind, c):
+        return p.spmv if kind == "spmv" else (p.fwd[c] if kind == "fwd" else p.bwd[c])
+
+    # ---------------------------------------------------------------- halo
+    def exchange(self, kind, c, vecs):
+        """Deliver the owners' values of `vecs` (one extended vector per local
+        rank) into the peers' halo slices for exchange step (kind, c)."""
+        exs = [self._ex(p, kind, c) for p in self.parts]
+        if all(ex.n_send == 0 and not ex.recvs for ex in exs):
+            return
+        for i, ex in enumerate(exs):
+            self.ops[i].pack((kind, c), ex, vecs[i], self.sendbuf.get((kind, c, i)))
+        p2p = []
+        for i, (p, ex) in enumerate(zip(self.parts, exs)):
+            buf = self.sendbuf.get((kind, c, i))
+            for m in ex.sends:
+                self.bytes_sent += 8 * m.count
+                j = self.local.get(m.peer)
+                if j is not None:
+                    # in-process peer: find its matching receive slot
+                    rm = next(r for r in exs[j].recvs if r.peer == p.rank)
+                    assert rm.count == m.count
+                    self.ops[j].copy_range(vecs[j], rm.offset, buf, m.offset, m.count)
+                else:
+                    p2p.append(self.dist.P2POp(self.dist.isend, buf[m.offset:m.offset + m.count],
+                                               m.peer, self.group))
+            for rm in ex.recvs:
+                if rm.peer not in self.local:
+                    p2p.append(self.dist.P2POp(self.dist.irecv,
+                                               vecs[i][rm.offset:rm.offset + rm.count],
+                                               rm.peer, self.group))
+        if p2p:
+            for req in self.dist.batch_isend_irecv(p2p):
+                req.wait()
+        self.exchanges += 1
+
+    # ---------------------------------------------------------------- reductions
+    def allreduce(self, scals, slots):
+        """Sum the given scalar slots over all ranks, result on every rank."""
+        if len(scals) > 1:
+            for i in range(1, len(scals)):
+                self.ops[0].add_scal(scals[0], scals[i], slots)
+        if self.dist is not None:
+            lo, hi = min(slots), max(slots) + 1
+            self.dist.all_reduce(scals[0][lo:hi], group=self.group)
+        for i in range(1, len(scals)):
+            self.ops[i].set_scal(scals[i], scals[0], slots)
+
+    # ---------------------------------------------------------------- operators
+    def sweep(self, forward, src, dst):
+        """One substitution sweep on all local ranks with the per-color halo
+        exchange (src/precond.py:377-392)."""
+        order = range(self.n_c) if forward else range(self.n_c - 1, -1, -1)
+        for c in order:
+            for i in range(len(self.parts)):
+                self.ops[i].sweep_phase(forward, c, src[i], dst[i])
+            self.exchange("fwd" if forward else "bwd", c, dst)
+
+    def precond(self, r, y, z):
+        self.sweep(True, r, y)
+        self.sweep(False, y, z)
+
+    def spmv(self, x, out):
+        self.exchange("spmv", -1, x)
+        for i in range(len(self.parts)):
+            self.ops[i].spmv(x[i], out[i])
+
+    # ---------------------------------------------------------------- PCG
+    def pcg(self, b_loc, tol=1e-7, max_iters=50000):
+        """src/solver.py:157-193 over the partition.
+
+        b_loc: per local rank, the local rhs (length n_loc; backend vectors).
+        Returns (x per local rank, iterations, history, converged).
+        """
+        R = range(len(self.parts))
+        O = self.ops
+        V = lambda: [O[i].vec() for i in R]  # noqa: E731
+        x, r, y, z, p, ap = V(), V(), V(), V(), V(), V()
+        sc = [O[i].scalars() for i in R]
+        for i in R:
+            O[i].fill_zero(x[i])
+            O[i].copy(r[i], b_loc[i])
+            O[i].dot(r[i], r[i], sc[i], BB)
+        self.allreduce(sc, [BB])
+        bnorm = math.sqrt(O[0].read(sc[0], [BB])[0])
+        if bnorm == 0.0:
+            return x, 0, [0.0], True
+        history = [1.0]
+        self.precond(r, y, z)
+        for i in R:
+            O[i].copy(p[i], z[i])
+            O[i].dot(r[i], z[i], sc[i], RZ0)
+        self.allreduce(sc, [RZ0])
+        rz, rzn = RZ0, RZ1
+        it, converged = 0, False
+        for j in range(1, max_iters + 1):
+            self.spmv(p, ap)
+            for i in R:
+                O[i].dot(p[i], ap[i], sc[i], PAP)
+            self.allreduce(sc, [PAP])
+            for i in R:
+                O[i].update_xr(sc[i], rz, PAP, p[i], ap[i], x[i], r[i], RR)
+            self.allreduce(sc, [RR])
+            pap, rr = O[0].read(sc[0], [PAP, RR])
+            if pap <= 0.0:
+                from .solver import CgBreakdownError
+                raise CgBreakdownError(j, pap)
+            rel = math.sqrt(rr) / bnorm
+            history.append(rel)
+            it = j
+            if rel < tol:
+                converged = True
+                break
+            self.precond(r, y, z)
+            for i in R:
+                O[i].dot(r[i], z[i], sc[i], rzn)
+            self.allreduce(sc, [rzn])
+            for i in R:
+                O[i].update_p(sc[i], rzn, rz, z[i], p[i])
+            rz, rzn = rzn, rz
+        return x, it, history, converged
+
+
+def partition_setup(setup, world, ranks=None):
+    """RankParts of a prepared single-system HBMC Setup (solver.prepare)."""
+    from .matrix import csr_to_sell
+    sf, hl = setup.factor, setup.layout
+    a_sell = csr_to_sell(setup.a_sys, sf.w, want_col64=True)
+    return partition_hbmc(sf.lower, sf.upper, a_sell, sf.inv_diag, hl.color_lvl1_ranges,
+                          sf.b_s, sf.w, world, ranks)
+
+
+def pcg_partitioned(a, b, cfg, world, matrix_name="", group=None):
+    """HBMC ICCG with the rows partitioned over `world` ranks.
+
+    Without torch.distributed: all `world` ranks are driven by this process
+    on the current device (virtual ranks).  Under torch.distributed with
+    world_size == world: this process drives its own rank; every rank
+    returns the full solution (gathered on the host) and the same report.
+    Returns (x in the original ordering, SolveReport).
+    """
+    from . import solver
+    cfg.validate()
+    if cfg.ordering != "hbmc":
+        raise ValueError("pcg_partitioned: only the hbmc ordering partitions")
+    t0 = time.perf_counter()
+    setup = solver.prepare(a, b, cfg)
+    dist = None
+    try:
+        import torch.distributed as td
+        if td.is_initialized() and td.get_world_size(group) > 1:
+            dist = td
+    except ImportError:
+        pass
+    ranks = [dist.get_rank(group)] if dist is not None else None
+    if dist is not None and dist.get_world_size(group) != world:
+        raise ValueError("pcg_partitioned: world != torch.distributed world size")
+    parts = partition_setup(setup, world, ranks)
+    ops = [CudaRankOps(p) for p in parts]
+    drv = DistHbmc(parts, ops, group)
+    b_loc = [ops[i].from_host(setup.b_sys[p.rows]) for i, p in enumerate(parts)]
+    ops[0].t.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    xs, it, hist, conv = drv.pcg(b_loc, cfg.tol, cfg.max_iters)
+    x_sys = np.zeros(setup.a_sys.n)
+    for i, p in enumerate(parts):
+        x_sys[p.rows] = ops[i].to_host(xs[i])
+    if dist is not None:
+        # every row is owned by exactly one rank: a sum assembles x everywhere
+        xt = ops[0].t.from_numpy(x_sys)
+        if dist.get_backend(group) == "nccl":
+            xt = xt.cuda()
+        dist.all_reduce(xt, group=group)
+        x_sys = xt.cpu().numpy()
+    t_solve = time.perf_counter() - t1
+    for o in ops:
+        o.close()
+    x_out = x_sys[setup.old_positions]
+    applies = it if conv else 1 + it
+    barrier_total = applies * 2 * max(setup.n_c - 1, 0)
+    rep = solver.SolveReport(matrix_name, cfg.ordering, cfg.b_s, cfg.w, setup.n_c, int(it),
+                             bool(conv), t_setup, t_solve, [float(v) for v in hist],
+                             barrier_total, setup.n_dummy)
+    return x_out, rep

@@ -1,0 +1,6 @@
+#!/bin/bash
+# GPU parity suite with durations (round evidence for the partitioned path).
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=15 ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -30 gpurun_out/pytest_gpu.log

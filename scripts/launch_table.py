@@ -17,7 +17,7 @@ part = data[len(data) // 2:] if "--second-half" in sys.argv else data
 agg = collections.OrderedDict()
 for d in part:
     v = float(d["Metric Value"].replace(",", ""))
-    v = {"nsecond": v / 1e3, "usecond": v, "msecond": v * 1e3}.get(d["Metric Unit"], v)
+    v = {"nsecond": v / 1e3, "ns": v / 1e3, "usecond": v, "us": v, "msecond": v * 1e3, "ms": v * 1e3}.get(d["Metric Unit"], v)
     k = d["Kernel Name"].split("(")[0][:70]
     agg.setdefault(k, [0, 0.0])
     agg[k][0] += 1

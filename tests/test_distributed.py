@@ -1,0 +1,261 @@
+"""Row-partitioned HBMC ICCG on CPU: partition structure,
+exchange schedule and the distributed iteration.
+
+The per-rank compute here is the CPU oracle (test infrastructure) behind the
+same per-rank ops interface the product's CUDA backend implements, so these
+tests check the partition + exchange + reduction logic, not the kernels:
+
+* virtual ranks (G ranks in one process, in-process halo copies): the
+  partitioned forward / backward sweeps and SpMV are BITWISE equal to the
+  reference's unpartitioned outputs (golden y, z, A x), for G = 2, 3, 5;
+* world_size-2 gloo: two processes, halo messages through
+  torch.distributed batch_isend_irecv and dot all-reduces, PCG iterations
+  within +-1 of the reference and x within 1e-10.
+The GPU counterparts are in tests/test_gpu_parity.py.
+"""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1908_00741_b200 as P
+from conftest import golden_matrix, load_golden, rel_err
+from oracle import oracle as O
+from paper_1908_00741_b200 import distributed as D
+from paper_1908_00741_b200 import partition, problems, solver
+
+CASES = ["knn3000_b4_w32", "var7_16_b8_w32", "s27_10_b8_w32", "grid16_b4_w2",
+         "rand500_b8_w4", "lap7_12_b4_w8"]
+
+
+class OracleRankOps:
+    """CPU per-rank backend over the C oracle (test infrastructure only)."""
+
+    def __init__(self, part):
+        self.part = part
+        self.n = part.n_loc
+        L, U, A = part.L, part.U, part.A
+        self.L = (L.slice_ptr, L.slice_len, L.col_idx, L.vals)
+        self.U = (U.slice_ptr, U.slice_len, U.col_idx, U.vals)
+        self.A = (A.slice_ptr, A.slice_len, A.col_idx, A.vals)
+        self.inv_d = np.ascontiguousarray(part.inv_d)
+
+    def vec(self, n=None):
+        return torch.zeros(self.part.n_ext if n is None else n, dtype=torch.float64)
+
+    def scalars(self):
+        return torch.zeros(D.N_SCAL, dtype=torch.float64)
+
+    def from_host(self, a):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).copy())
+
+    def to_host(self, v, n=None):
+        return v[: self.n if n is None else n].numpy().copy()
+
+    def sweep_phase(self, forward, c, src, dst):
+        cr = self.part.color_lvl1_ranges
+        fn = O.LIB.or_fwd_sell_range if forward else O.LIB.or_bwd_sell_range
+        sp, sl, ci, v = self.L if forward else self.U
+        fn(sp, sl, ci, v, self.inv_d, src.numpy(), dst.numpy(), self.part.w, self.part.b_s,
+           int(cr[c]), int(cr[c + 1]))
+
+    def spmv(self, x, out):
+        sp, sl, ci, v = self.A
+        res = np.empty(self.n)
+        O.LIB.or_spmv_sell(self.n // self.part.w, sp, sl, ci, v, self.part.w, x.numpy(), res)
+        out[: self.n] = torch.from_numpy(res)
+
+    def pack(self, key, ex, src, buf):
+        if ex.n_send:
+            buf[:] = src[torch.from_numpy(ex.send_idx.astype(np.int64))]
+
+    def copy_range(self, dst, doff, src, soff, cnt):
+        dst[doff:doff + cnt] = src[soff:soff + cnt]
+
+    def dot(self, u, v, scal, slot):
+        scal[slot] = float(np.dot(u[: self.n].numpy(), v[: self.n].numpy()))
+
+    def update_xr(self, scal, num, den, p, ap, x, r, rr_slot):
+        alpha = float(scal[num]) / float(scal[den])
+        n = self.n
+        x[:n] += alpha * p[:n]
+        r[:n] -= alpha * ap[:n]
+        scal[rr_slot] = float(np.dot(r[:n].numpy(), r[:n].numpy()))
+
+    def update_p(self, scal, num, den, z, p):
+        beta = float(scal[num]) / float(scal[den])
+        p[: self.n] = z[: self.n] + beta * p[: self.n]
+
+    def copy(self, dst, src):
+        dst[: self.n] = src[: self.n]
+
+    def fill_zero(self, v):
+        v.zero_()
+
+    def read(self, scal, slots):
+        return [float(scal[s]) for s in slots]
+
+    def add_scal(self, dst, src, slots):
+        for s in slots:
+            dst[s] += src[s]
+
+    def set_scal(self, dst, src, slots):
+        for s in slots:
+            dst[s] = src[s]
+
+
+def _setup(name):
+    a, bs, w, rhs_kind = golden_matrix(name)
+    b = np.ones(a.n) if rhs_kind == "ones" else problems.rhs(a)[1]
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    return a, b, cfg, solver.prepare(a, b, cfg)
+
+
+def _scatter(parts, glob):
+    return [torch.from_numpy(np.concatenate([glob[p.rows], np.zeros(p.n_halo)])) for p in parts]
+
+
+def _gather(parts, vecs, n):
+    out = np.full(n, np.nan)
+    for p, v in zip(parts, vecs):
+        out[p.rows] = v[: p.n_loc].numpy()
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("name", CASES)
+def test_partition_structure(name, world):
+    a, b, cfg, st = _setup(name)
+    parts = D.partition_setup(st, world)
+    hl = st.layout
+    n_pad = hl.n_pad
+    rows = np.concatenate([p.rows for p in parts])
+    assert np.array_equal(np.sort(rows), np.arange(n_pad))      # every row owned once
+    span = cfg.b_s * cfg.w
+    for p in parts:
+        assert p.n_loc == p.lvl1.shape[0] * span
+        assert p.color_lvl1_ranges[-1] == p.lvl1.shape[0]
+        for M in (p.L, p.U, p.A):
+            assert M.col_idx.size == 0 or M.col_idx.max() < p.n_ext
+            assert M.n_slices * cfg.w == p.n_loc
+        # owned level-1 blocks of one color: the rule of src/precond.py:153-160
+        for c in range(hl.n_c):
+            lo, hi = hl.color_lvl1_ranges[c], hl.color_lvl1_ranges[c + 1]
+            a0, a1 = partition.chunk_bounds(int(lo), int(hi), world)[p.rank]
+            got = p.lvl1[p.color_lvl1_ranges[c]:p.color_lvl1_ranges[c + 1]]
+            assert np.array_equal(got, np.arange(a0, a1))
+        # halo rows are remote, unique
+        assert np.unique(p.halo_rows).shape[0] == p.n_halo
+        assert not np.isin(p.halo_rows, p.rows).any()
+    # every message's send list and receive slot agree on length and content
+    for kind in ("fwd", "bwd", "spmv"):
+        for c in (range(hl.n_c) if kind != "spmv" else [-1]):
+            for p in parts:
+                ex = D.DistHbmc._ex(p, kind, c)
+                for m in ex.sends:
+                    q = parts[m.peer]
+                    rm = [r for r in D.DistHbmc._ex(q, kind, c).recvs if r.peer == p.rank]
+                    assert len(rm) == 1 and rm[0].count == m.count
+                    sent_rows = p.rows[ex.send_idx[m.offset:m.offset + m.count]]
+                    recv_rows = q.halo_rows[rm[0].offset - q.n_loc:rm[0].offset - q.n_loc + m.count]
+                    assert np.array_equal(sent_rows, recv_rows)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("name", CASES)
+def test_partitioned_sweeps_and_spmv_bitwise(name, world):
+    """Virtual ranks: partitioned sweeps / SpMV == the reference's outputs."""
+    g = load_golden(name)
+    a, b, cfg, st = _setup(name)
+    parts = D.partition_setup(st, world)
+    drv = D.DistHbmc(parts, [OracleRankOps(p) for p in parts])
+    n = st.layout.n_pad
+    r = _scatter(parts, g["r"])
+    y = [torch.zeros(p.n_ext, dtype=torch.float64) for p in parts]
+    z = [torch.zeros(p.n_ext, dtype=torch.float64) for p in parts]
+    drv.sweep(True, r, y)
+    assert np.array_equal(_gather(parts, y, n), g["y"])
+    drv.sweep(False, y, z)
+    assert np.array_equal(_gather(parts, z, n), g["z"])
+    # exchanges: n_c - 1 per sweep (the reference's barriers) when any halo exists
+    assert drv.exchanges <= 2 * max(st.n_c - 1, 0)
+    x = _scatter(parts, g["spmv_x"])
+    ax = [torch.zeros(p.n_ext, dtype=torch.float64) for p in parts]
+    drv.spmv(x, ax)
+    assert np.array_equal(_gather(parts, ax, n)[: g["spmv_sell"].shape[0]], g["spmv_sell"])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32", "s27_10_b8_w32"])
+def test_partitioned_pcg_virtual_ranks(name, world):
+    g = load_golden(name)
+    a, b, cfg, st = _setup(name)
+    parts = D.partition_setup(st, world)
+    ops = [OracleRankOps(p) for p in parts]
+    drv = D.DistHbmc(parts, ops)
+    xs, it, hist, conv = drv.pcg([o.from_host(st.b_sys[p.rows]) for o, p in zip(ops, parts)],
+                                 cfg.tol, cfg.max_iters)
+    x = _gather(parts, xs, st.layout.n_pad)[st.old_positions]
+    assert conv == bool(g["pcg_hbmc_converged"])
+    assert abs(it - int(g["pcg_hbmc_iters"])) <= 1
+    assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
+    href = g["pcg_hbmc_hist"]
+    m = max(min(len(hist), href.shape[0]) - 2, 0)
+    assert np.max(np.abs(np.asarray(hist[:m]) - href[:m]) / href[:m]) <= 1e-6
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, name, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b, cfg, st = _setup(name)
+        parts = D.partition_setup(st, world, ranks=[rank])
+        ops = [OracleRankOps(parts[0])]
+        drv = D.DistHbmc(parts, ops)
+        assert drv.dist is not None
+        xs, it, hist, conv = drv.pcg([ops[0].from_host(st.b_sys[parts[0].rows])],
+                                     cfg.tol, cfg.max_iters)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), rows=parts[0].rows,
+                 x=xs[0][: parts[0].n_loc].numpy(), it=it, hist=np.asarray(hist), conv=conv,
+                 exchanges=drv.exchanges, sent=drv.bytes_sent)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32"])
+def test_partitioned_pcg_gloo_world2(name, tmp_path):
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_gloo_worker, args=(world, _free_port(), name, str(tmp_path)), nprocs=world,
+             join=True)
+    g = load_golden(name)
+    a, b, cfg, st = _setup(name)
+    res = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    # both ranks took identical decisions
+    assert res[0]["it"] == res[1]["it"]
+    assert np.array_equal(res[0]["hist"], res[1]["hist"])
+    assert all(r["sent"] > 0 for r in res)
+    x_sys = np.full(st.layout.n_pad, np.nan)
+    for r in res:
+        x_sys[r["rows"]] = r["x"]
+    x = x_sys[st.old_positions]
+    assert abs(int(res[0]["it"]) - int(g["pcg_hbmc_iters"])) <= 1
+    assert bool(res[0]["conv"]) == bool(g["pcg_hbmc_converged"])
+    assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
+    h = res[0]["hist"]
+    href = g["pcg_hbmc_hist"]
+    m = max(min(len(h), href.shape[0]) - 2, 0)
+    assert math.isclose(h[0], href[0])
+    assert np.max(np.abs(h[:m] - href[:m]) / href[:m]) <= 1e-6

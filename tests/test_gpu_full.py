@@ -1,0 +1,171 @@
+"""B200 parity at the BASELINE configs' full sizes, and the row-partitioned
+solve on the device.
+
+* Full-size ICCG (configs 2, 3, 4): permutation hash, iteration count within
+  +-1 and residual history against the reference's own run
+  (tests/golden/config{2,3,4}_digest.json, made by make_golden.py from
+  trilab itself), solution samples within 1e-10 relative.
+* Partitioned solve with G virtual ranks on one device (each rank's sweeps
+  and SpMV are the plan kernels on its local system; halo exchange by
+  device copies, serialised on one stream -- no rank waits on another
+  inside a kernel): sweeps and SpMV BITWISE equal to the reference's
+  outputs, PCG within +-1 iteration / 1e-10.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_matrix, load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1908_00741_b200 as P
+    return P
+
+
+def sha(x):
+    return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+
+
+def _digest(cfg_id):
+    with open(os.path.join(GOLDEN, f"config{cfg_id}_digest.json")) as fh:
+        return json.load(fh)
+
+
+def _check_against_digest(rep, x, dg):
+    ref = dg["hbmc"]
+    assert rep.converged == ref["converged"]
+    assert abs(rep.iterations - ref["iterations"]) <= 1, (rep.iterations, ref["iterations"])
+    h = np.asarray(rep.residual_history)
+    href = np.asarray(ref["history"])
+    assert h[0] == href[0]
+    # Dots are reduced in a different order than numpy's BLAS ddot; in a long
+    # solve CG amplifies that roundoff (config 2: history within 1e-9 up to
+    # iteration ~70, then drifting by up to ~13 % on the plateau before
+    # convergence).  The bar is the iteration count and the solution; the
+    # early history pins that the same iteration is being run.
+    m = min(h.shape[0], href.shape[0], 40)
+    assert np.max(np.abs(h[:m] - href[:m]) / href[:m]) <= 1e-6
+    xs = x[::ref["x_sample_stride"]]
+    xr = np.asarray(ref["x_sample"])
+    assert xs.shape == xr.shape
+    assert rel_err(xs, xr) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3, 4])
+def test_full_config_iccg_matches_reference(P, cfg_id):
+    from paper_1908_00741_b200 import problems
+    dg = _digest(cfg_id)
+    label, gen, bs, w = problems.CONFIGS[cfg_id]
+    a = gen()
+    assert a.n == dg["n"] and a.nnz == dg["nnz"]
+    _, b = problems.rhs(a)
+    x, rep = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell"))
+    _check_against_digest(rep, x, dg)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_full_config2_partitioned_iccg(P, world):
+    from paper_1908_00741_b200 import distributed, problems
+    dg = _digest(2)
+    label, gen, bs, w = problems.CONFIGS[2]
+    a = gen()
+    _, b = problems.rhs(a)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    x, rep = distributed.pcg_partitioned(a, b, cfg, world)
+    _check_against_digest(rep, x, dg)
+
+
+CASES = ["knn3000_b4_w32", "var7_16_b8_w32", "aniso12_b16_w32", "grid32_b8_w4",
+         "rand500_b8_w4", "lap7_12_b4_w8"]
+
+
+def _parts(P, name, world):
+    from paper_1908_00741_b200 import distributed, problems, solver
+    a, bs, w, rhs_kind = golden_matrix(name)
+    b = np.ones(a.n) if rhs_kind == "ones" else problems.rhs(a)[1]
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    st = solver.prepare(a, b, cfg)
+    parts = distributed.partition_setup(st, world)
+    ops = [distributed.CudaRankOps(p) for p in parts]
+    return a, b, cfg, st, parts, ops, distributed.DistHbmc(parts, ops)
+
+
+def _scatter(ops, parts, glob):
+    return [o.from_host(np.concatenate([glob[p.rows], np.zeros(p.n_halo)]))
+            for o, p in zip(ops, parts)]
+
+
+def _gather(ops, parts, vecs, n):
+    out = np.full(n, np.nan)
+    for o, p, v in zip(ops, parts, vecs):
+        out[p.rows] = o.to_host(v)
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", CASES)
+def test_partitioned_sweeps_spmv_bitwise_on_device(P, name, world):
+    import torch
+    g = load_golden(name)
+    a, b, cfg, st, parts, ops, drv = _parts(P, name, world)
+    n = st.layout.n_pad
+    nan = lambda p: torch.full((p.n_ext,), float("nan"), dtype=torch.float64,  # noqa: E731
+                               device="cuda")
+    r = _scatter(ops, parts, g["r"])
+    y = [nan(p) for p in parts]
+    z = [nan(p) for p in parts]
+    drv.sweep(True, r, y)
+    drv.sweep(False, y, z)
+    torch.cuda.synchronize()
+    assert np.array_equal(_gather(ops, parts, y, n), g["y"])
+    assert np.array_equal(_gather(ops, parts, z, n), g["z"])
+    x = _scatter(ops, parts, g["spmv_x"])
+    ax = [nan(p) for p in parts]
+    drv.spmv(x, ax)
+    got = _gather(ops, parts, ax, n)
+    assert np.array_equal(got[: g["spmv_sell"].shape[0]], g["spmv_sell"])
+    for o in ops:
+        o.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32", "aniso12_b16_w32"])
+def test_partitioned_pcg_on_device(P, name, world):
+    g = load_golden(name)
+    a, b, cfg, st, parts, ops, drv = _parts(P, name, world)
+    xs, it, hist, conv = drv.pcg([o.from_host(st.b_sys[p.rows]) for o, p in zip(ops, parts)],
+                                 cfg.tol, cfg.max_iters)
+    x = _gather(ops, parts, xs, st.layout.n_pad)[st.old_positions]
+    assert conv == bool(g["pcg_hbmc_converged"])
+    assert abs(it - int(g["pcg_hbmc_iters"])) <= 1
+    assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
+    href = g["pcg_hbmc_hist"]
+    m = max(min(len(hist), href.shape[0]) - 2, 0)
+    assert np.max(np.abs(np.asarray(hist[:m]) - href[:m]) / href[:m]) <= 1e-6
+    for o in ops:
+        o.close()
+
+
+def test_partitioned_public_entry_point(P):
+    """pcg_partitioned (virtual ranks) == the reference's report on a golden."""
+    from paper_1908_00741_b200 import distributed, problems
+    name = "var7_16_b8_w32"
+    g = load_golden(name)
+    a, bs, w, _ = golden_matrix(name)
+    _, b = problems.rhs(a)
+    x, rep = distributed.pcg_partitioned(a, b, P.CgConfig(ordering="hbmc", b_s=bs, w=w,
+                                                          spmv_format="sell"), 2)
+    assert abs(rep.iterations - int(g["pcg_hbmc_iters"])) <= 1
+    assert rep.barrier_total == int(g["pcg_hbmc_barriers"])
+    assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
