@@ -26,8 +26,12 @@ iccg     = full PCG solve to 1e-7 on the device (one CUDA-graph launch).
 cpu_baseline = the CPU oracle port of the reference path (oracle/), all host
            threads, bounded sample of the same sweep workload (rank 0, N=1).
 
-N > 1: every rank solves its own replica of the problem (no data-path
-collective); timing is the max over ranks (scaling "weak").
+N > 1 (torchrun, one rank per GPU, NCCL): the row-partitioned solve of
+SURVEY 8(e) -- every color's level-1 blocks split over the ranks, one halo
+exchange (NCCL P2P over NVLink) after every color phase, CG dots all-reduced.
+The problem is fixed as N grows (scaling "strong"); value = the whole
+system's algorithmic sweep bytes / max-over-ranks device time.
+`--mode replicas` instead runs N independent replicas (scaling "weak").
 """
 
 import argparse
@@ -294,6 +298,32 @@ def run_ours(args, rank, world, local_rank):
         tot_ms = sum(lt)
         n_launch = len(lt)
     achieved = tot_b / (tot_ms / 1e3) / 1e9
+    traffic, traffic_src = args.traffic, "--traffic" if args.traffic else None
+    if traffic is None:
+        tp = os.path.join(HERE, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as fh:
+                tj = json.load(fh).get(f"config{args.config}", {})
+            key = "persistent_precond" if pinfo["precond"] else "per_phase"
+            if key in tj:
+                traffic = tj[key]["dram_bytes_per_launch"]
+                traffic_src = tj[key]["source"]
+
+    # ---------------- SpMV kernel alone (second hot kernel of the iteration)
+    ap_dev = torch.empty_like(r)
+    tsp = Timer(torch, stream, args.warmup + args.steps)
+    for _ in range(args.warmup + args.steps):
+        flush()
+        tsp.start()
+        plan.spmv(r, ap_dev, sptr)
+        tsp.stop()
+    sp_ms = tsp.times_ms()[args.warmup:]
+    sp_us = 1e3 * sum(sp_ms) / len(sp_ms)
+    sp_bytes = spmv_bytes(int(a.nnz), a.n)
+    spmv_line = {"kernel": "spmv_sell (thread per row, 8 slots in flight)",
+                 "algorithmic_bytes": sp_bytes, "avg_us": sp_us,
+                 "achieved": sp_bytes / (sp_us / 1e6) / 1e9, "peak": peak, "unit": "GB/s",
+                 "frac": sp_bytes / (sp_us / 1e6) / 1e9 / peak}
 
     # ---------------- e2e through the public API (host buffers)
     r_host = torch.from_numpy(np.random.default_rng(0).standard_normal(n_pad)).pin_memory()
@@ -379,7 +409,7 @@ def run_ours(args, rank, world, local_rank):
                          "frac": achieved / peak, "peak_source": peak_src,
                          "launches": n_launch, "avg_launch_us": 1e3 * tot_ms / max(1, n_launch),
                          "algorithmic_bytes_per_launch": tot_b / max(1, n_launch),
-                         "traffic": args.traffic,
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "per_phase_kernels": per_phase},
             "cpu_baseline": cb,
             "e2e": {"value": e2e_val, "unit": "GB/s",
@@ -400,12 +430,123 @@ def run_ours(args, rank, world, local_rank):
                      "e2e_solve_ms": 1e3 * min(t_e2e_solve),
                      "setup_host_s": t_host, "setup_total_s": t_setup,
                      "generate_s": t_gen},
-            "spmv_bytes_per_call": spmv_bytes(int(a.nnz), a.n),
+            "spmv": spmv_line,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
     return line
+
+
+def run_partitioned(args, rank, world, local_rank):
+    """one rank per GPU, rows of every color split over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1908_00741_b200 as P
+    from paper_1908_00741_b200 import distributed as D
+    from paper_1908_00741_b200 import solver
+
+    dev = torch.device("cuda", local_rank)
+    label, a, xs, b, bs, w, t_gen = build_problem(args.config)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    t0 = time.perf_counter()
+    setup = solver.prepare(a, b, cfg)
+    part = D.partition_setup(setup, world, ranks=[rank])[0]
+    ops = D.CudaRankOps(part)
+    drv = D.DistHbmc([part], [ops])
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    hl = setup.layout
+    nnz_l = int((a.nnz - a.n) // 2)
+    step_bytes = 2 * sweep_bytes(nnz_l, a.n)
+    stream = torch.cuda.current_stream(dev)
+    flush_src = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    flush_dst = torch.empty((), dtype=torch.float64, device=dev)
+
+    def flush():
+        torch.sum(flush_src, dim=0, out=flush_dst)
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    r_glob = np.random.default_rng(0).standard_normal(hl.n_pad)
+    r = [ops.from_host(np.concatenate([r_glob[part.rows], np.zeros(part.n_halo)]))]
+    y, z = [ops.vec()], [ops.vec()]
+    for _ in range(args.warmup):
+        flush()
+        drv.precond(r, y, z)
+    barrier()
+    tm = Timer(torch, stream, args.steps)
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush()
+            tm.start()
+            drv.precond(r, y, z)
+            tm.stop()
+        dev_ms = sum(tm.times_ms())
+    barrier()
+    # e2e: local r from pinned host, z back to pinned host
+    r_host = torch.from_numpy(r_glob[part.rows].copy()).pin_memory()
+    z_host = torch.empty(part.n_loc, dtype=torch.float64).pin_memory()
+    te = Timer(torch, stream, args.steps)
+    for _ in range(args.steps):
+        flush()
+        te.start()
+        r[0][:part.n_loc].copy_(r_host, non_blocking=True)
+        drv.precond(r, y, z)
+        z_host.copy_(z[0][:part.n_loc], non_blocking=True)
+        te.stop()
+    e2e_ms = sum(te.times_ms())
+    barrier()
+    # ICCG time-to-solution (host-timed around a synchronised solve)
+    b_loc = [ops.from_host(setup.b_sys[part.rows])]
+    drv.pcg(b_loc, cfg.tol, cfg.max_iters)
+    barrier()
+    t1 = time.perf_counter()
+    xs_loc, it, hist, conv = drv.pcg(b_loc, cfg.tol, cfg.max_iters)
+    torch.cuda.synchronize()
+    solve_ms = 1e3 * (time.perf_counter() - t1)
+
+    def mx(v):
+        tt = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    dev_ms_max, e2e_ms_max, solve_ms_max = mx(dev_ms), mx(e2e_ms), mx(solve_ms)
+    value = step_bytes * args.steps / (dev_ms_max / 1e3) / 1e9
+    peak, peak_src = load_peaks()
+    if rank == 0:
+        per_gpu = value / world
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, SURVEY Appendix B)",
+            "config": {"workload": f"config{args.config} {label} b_s={bs} w={w}",
+                       "N": a.n, "n_pad": hl.n_pad, "nnz_L": nnz_l, "n_c": hl.n_c,
+                       "bytes_per_step": step_bytes,
+                       "l2": "flushed before every timed step (256 MiB read)",
+                       "parallelism": f"row-partitioned x{world} (per-color halo over NCCL P2P)",
+                       "halo_rows_rank0": part.n_halo, "rows_rank0": part.n_loc},
+            "roofline": {"bound": "hbm", "kernel": "per-rank HBMC sweep phases + halo exchange",
+                         "achieved": per_gpu, "peak": peak, "unit": "GB/s",
+                         "frac": per_gpu / peak, "peak_source": peak_src, "traffic": None},
+            "cpu_baseline": None,
+            "e2e": {"value": step_bytes * args.steps / (e2e_ms_max / 1e3) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * part.n_loc, "d2h_bytes_per_step": 8 * part.n_loc,
+                    "ms_per_step": e2e_ms_max / args.steps},
+            "gpu_launches": args.steps * (2 * hl.n_c + 2 * max(hl.n_c - 1, 0)),
+            "clocks": clk.summary(),
+            "iccg": {"iterations": int(it), "converged": bool(conv),
+                     "time_to_solution_ms": solve_ms_max, "setup_total_s": t_setup,
+                     "exchanges_per_precond": 2 * max(hl.n_c - 1, 0)},
+        }
+        print(json.dumps(line), flush=True)
+    ops.close()
+    dist.barrier()
 
 
 def main():
@@ -416,6 +557,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="partitioned", choices=["partitioned", "replicas"],
+                    help="N > 1: row-partitioned solve (default) or independent replicas")
+    ap.add_argument("--force-partitioned", action="store_true",
+                    help="run the partitioned path even at N = 1 (code-path check)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (profiles/)")
     args = ap.parse_args()
@@ -426,13 +571,20 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
-    if world > 1:
+    partitioned = args.mode == "partitioned" and (world > 1 or args.force_partitioned)
+    if world > 1 or partitioned:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
-    run_ours(args, rank, world, local_rank)
-    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local_rank))
+    if partitioned:
+        run_partitioned(args, rank, world, local_rank)
+    else:
+        run_ours(args, rank, world, local_rank)
+    if world > 1 or partitioned:
         import torch.distributed as dist
         dist.destroy_process_group()
 

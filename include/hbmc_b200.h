@@ -318,6 +318,18 @@ int tb_dev_cg_xr(int64_t n, double *s, int32_t num, int32_t den, const double *p
 int tb_dev_cg_p(int64_t n, const double *s, int32_t num, int32_t den, const double *z,
                 double *p, void *stream);
 
+/* K/numba_backend.py:40-79 ic0_factor on the device, bitwise, for a system
+ * in HBMC order (src/precond.py:179-200 with layout "hbmc"): one launch per
+ * color, thread per (level-1 block, lane) walking its b_s rows.  lrp / lci /
+ * lvals: strictly-lower CSR of A (device; lvals overwritten with L), adiag =
+ * a_ii (1 + shift) (device), d / inv_d outputs (device), pivot_ws: n doubles
+ * of device scratch.  A non-positive pivot returns TB_EIC_BREAKDOWN with the
+ * first such row (the one the sequential reference stops at) and its pivot. */
+int tb_dev_ic0_hbmc(int64_t n, const int64_t *lrp, const int32_t *lci, double *lvals,
+                    const double *adiag, double *d, double *inv_d, int64_t w, int64_t b_s,
+                    int64_t n_c, const int64_t *color_lvl1_ranges, double *pivot_ws,
+                    int64_t *bad_row, double *bad_pivot, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

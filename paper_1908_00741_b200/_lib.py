@@ -109,6 +109,7 @@ _SIGS = {
     "tb_dev_dot": [i64, vp, vp, vp, i32, vp, vp],
     "tb_dev_cg_xr": [i64, vp, i32, i32, vp, vp, vp, vp, i32, vp, vp],
     "tb_dev_cg_p": [i64, vp, i32, i32, vp, vp, vp],
+    "tb_dev_ic0_hbmc": [i64, vp, vp, vp, vp, vp, vp, i64, i64, i64, vp, vp, P_i64, P_dbl, vp],
 }
 
 EXPORTED = sorted(_SIGS) + ["tb_last_error"]

@@ -41,6 +41,7 @@ using tb::fail;
 #include "sweep_reg.cuh"
 #include "sweep_ring.cuh"
 #include "sweep_tma.cuh"
+#include "spmv_tma.cuh"
 #include "persist.cuh"
 
 #define CU(call)                                                          \
@@ -411,8 +412,11 @@ __global__ void __launch_bounds__(kBlock)
 // __grid_constant__: device functions take `const Params &`; without it the
 // parameter block would be copied to local memory and every field access
 // would become a local load.
+#ifndef TB_PMINB
+#define TB_PMINB 2   // co-resident CTAs per SM the persistent kernel is built for
+#endif
 template <int KC, bool FLOW>
-__global__ void __launch_bounds__(persist::kThreads, 2)
+__global__ void __launch_bounds__(persist::kThreads, TB_PMINB)
     pcg_persistent(const __grid_constant__ persist::Params P) {
   extern __shared__ __align__(16) double psm[];
   const int T = blockDim.x, b_s = P.b_s;
@@ -760,6 +764,8 @@ struct tb_plan {
   unsigned char *small = nullptr;  // per level-1 block: short-chain bits
   unsigned long long *trace = nullptr;  // TB_TRACE=1: in-kernel phase stamps
   unsigned epoch = 1;
+  // TMA-staged SpMV (spmv_tma.cuh): 0 slices per chunk = not configured
+  int spmv_S = 0, spmv_cap = 0, spmv_D = 0, spmv_grid = 0;
 };
 
 namespace {
@@ -1120,7 +1126,22 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
   if (n <= 0) return TB_OK;
   if (pl->spmv_format == TB_SPMV_NONE)
     return fail(TB_EINVAL, "plan has no matrix A (preconditioner-only plan)");
-  if (pl->spmv_format == TB_SPMV_SELL) {
+  if (pl->spmv_format == TB_SPMV_SELL && !dot && pl->spmv_S > 0) {
+    spmv_tma::Params P;
+    P.n_slices = pl->A.n_slices;
+    P.slice_ptr = pl->A.slice_ptr;
+    P.slice_len = pl->A.slice_len;
+    P.col = pl->A.col;
+    P.val = pl->A.val;
+    P.x = x;
+    P.out = out;
+    P.S = pl->spmv_S;
+    P.cap = pl->spmv_cap;
+    P.D = pl->spmv_D;
+    P.n_chunks = (pl->A.n_slices + P.S - 1) / P.S;
+    spmv_tma::spmv_kernel<<<pl->spmv_grid, spmv_tma::kThreads,
+                            spmv_tma::smem_bytes(P.cap, P.D), s>>>(P);
+  } else if (pl->spmv_format == TB_SPMV_SELL) {
     if (dot)
       (pl->A.paired ? spmv_sell<true, true> : spmv_sell<true, false>)
           <<<reduce_grid(n, 1), kBlock, 0, s>>>(n, pl->A.slice_ptr, pl->A.slice_len,
@@ -1283,13 +1304,18 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   int per_sm = 1 << 30;
   for (bool flow : {false, true}) {  // the grid must be co-resident for either variant
     PersistFn fn = persist_fn(kc, flow);
-    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // per-function attribute shared by all plans: the device maximum, not
+    // this plan's size (a later plan with a smaller b_s must not shrink it)
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
     int ps = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, (int)T, smem));
     per_sm = ps < per_sm ? ps : per_sm;
   }
   if (per_sm < 1) return TB_OK;
-  if (per_sm > 2) per_sm = 2;
+  {
+    const int cap = env_int("TB_PERSIST_CTAS", TB_PMINB);
+    if (per_sm > cap) per_sm = cap;
+  }
   pl->persist_kc = kc;
   pl->persist_smem = smem;
   pl->persist_grid = per_sm * pl->num_sms;
@@ -1428,6 +1454,51 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   return TB_OK;
 }
 
+// TMA-staged SpMV (spmv_tma.cuh) for a width-32 SELL A in the plain layout:
+// the largest S <= 8 whose biggest chunk fits D = 4 stages in ~100 KB, grid
+// = co-resident CTAs.  TB_SPMV_TMA=0 keeps the thread-per-row kernel.
+int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
+  pl->spmv_S = 0;
+  if (env_int("TB_SPMV_TMA", 1) == 0 || h.width != 32 || pl->A.paired || h.n_slices <= 0)
+    return TB_OK;
+  if (h.slice_ptr[h.n_slices] > 0x7fffffffLL) return TB_OK;
+  const int D = env_int("TB_SPMV_D", 4);
+  const size_t budget = (size_t)env_int("TB_SPMV_KB", 100) * 1024;
+  for (int S = env_int("TB_SPMV_S", 8); S >= 1; S /= 2) {
+    long long cap = 0;
+    for (long long s0 = 0; s0 < h.n_slices; s0 += S) {
+      const long long s1 = s0 + S < h.n_slices ? s0 + S : h.n_slices;
+      const long long c = h.slice_ptr[s1] - h.slice_ptr[s0];
+      cap = c > cap ? c : cap;
+    }
+    cap = (cap + 31) / 32 * 32;
+    if (cap < 32) cap = 32;
+    const size_t sm = spmv_tma::smem_bytes((int)cap, D);
+    if (sm > budget) continue;
+    // S < 8 leaves warps of the CTA without a slice (long rows, e.g. the
+    // 27-point and kNN configs): the thread-per-row kernel is faster there
+    if (S < spmv_tma::kWarps && env_int("TB_SPMV_S", 0) == 0) return TB_OK;
+    // the attribute is per function, shared by every plan: set it to the
+    // device maximum once instead of this plan's size
+    int optin = 0;
+    CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
+    CU(cudaFuncSetAttribute(spmv_tma::spmv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            optin));
+    int per_sm = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_tma::spmv_kernel,
+                                                     spmv_tma::kThreads, sm));
+    if (per_sm < 1) return TB_OK;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
+    pl->spmv_S = S;
+    pl->spmv_cap = (int)cap;
+    pl->spmv_D = D;
+    pl->spmv_grid = per_sm * nsm;
+    return TB_OK;
+  }
+  return TB_OK;
+}
+
 int sync_in(tb_plan *pl, void *stream) {
   CU(cudaEventRecord(pl->ev_in, (cudaStream_t)stream));
   CU(cudaStreamWaitEvent(pl->stream, pl->ev_in, 0));
@@ -1506,6 +1577,7 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
                         d->A_sell.slice_ptr[d->A_sell.n_slices] <= 0x7fffffffLL;
     if ((rc = pair_a ? upload_sell_paired(pl->A, d->A_sell) : upload_sell(pl->A, d->A_sell)))
       return bail(rc);
+    if ((rc = configure_spmv_tma(pl, d->A_sell))) return bail(rc);
   } else {
     if ((rc = upload_csr(pl->Ac, d->A_csr))) return bail(rc);
   }

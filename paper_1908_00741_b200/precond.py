@@ -170,6 +170,60 @@ def ic0_factorize(a: CsrMatrix, shift=0.0, layout_tag="natural", kernels=None):
     return IcFactor(L, d, inv_d, float(shift), layout_tag, csr_transpose(L))
 
 
+def _check_hbmc_lower_structure(low, hl):
+    """Every strictly-lower (i, j) must be same level-1 block + same lane +
+    earlier step, or an earlier color (src/ordering.py:328-346): the
+    dependency structure the per-color device schedule relies on."""
+    w, span = hl.w, hl.w * hl.b_s
+    rows = np.repeat(np.arange(low.n, dtype=np.int64), np.diff(low.row_ptr))
+    cols = low.col_idx
+    ki, kj = rows // span, cols // span
+    same = ki == kj
+    ok_in = (rows % w == cols % w) & (cols < rows)
+    col_of = np.repeat(np.arange(hl.n_c, dtype=np.int64), np.diff(hl.color_lvl1_ranges))
+    ok_x = col_of[kj] < col_of[ki]
+    if not np.all(np.where(same, ok_in, ok_x)):
+        raise ValueError("ic0_factorize_device: matrix lacks the HBMC dependency structure")
+
+
+def ic0_factorize_device(a: CsrMatrix, hl, shift=0.0, layout_tag="hbmc"):
+    """ic0_factorize for a system already in HBMC order, computed on the B200
+    (csrc/ic0.cu: one launch per color).  Same IcFactor,
+    bitwise, same IcBreakdownError; `hl` is the HbmcLayout of `a`'s ordering.
+    """
+    from . import device
+    t = device.require_cuda()
+    if shift < 0:
+        raise ValueError("shift must be non-negative")
+    if (a.diag_ptr < 0).any():
+        bad = int(np.nonzero(a.diag_ptr < 0)[0][0])
+        raise ValueError(f"row {bad} has no diagonal entry")
+    if a.n != hl.n_pad:
+        raise ValueError("ic0_factorize_device: matrix is not in the layout's order")
+    _check_structural_symmetry(a)
+    low = _strict_tri(a, upper=False)
+    _check_hbmc_lower_structure(low, hl)
+    rp = device.to_device(low.row_ptr, np.int64)
+    ci = device.to_device(low.col_idx, np.int32)
+    lv = device.to_device(low.vals, np.float64)
+    ad = device.to_device(a.diagonal() * (1.0 + shift), np.float64)
+    d = t.empty(a.n, dtype=t.float64, device="cuda")
+    inv_d = t.empty_like(d)
+    ws = t.empty_like(d)
+    cr = np.ascontiguousarray(hl.color_lvl1_ranges, dtype=np.int64)
+    bad_row, pivot = _lib.i64(), _lib.dbl()
+    rc = LIB.tb_dev_ic0_hbmc(a.n, ptr(rp), ptr(ci), ptr(lv), ptr(ad), ptr(d), ptr(inv_d),
+                             hl.w, hl.b_s, hl.n_c, ptr(cr), ptr(ws), bad_row, pivot,
+                             device.current_stream())
+    if rc == _lib.TB_EIC_BREAKDOWN:
+        raise IcBreakdownError(bad_row.value, pivot.value)
+    check(rc)
+    L = CsrMatrix(a.n, low.row_ptr, low.col_idx, lv.cpu().numpy(),
+                  diag_ptr=np.full(a.n, -1, dtype=np.int64))
+    return IcFactor(L, d.cpu().numpy(), inv_d.cpu().numpy(), float(shift), layout_tag,
+                    csr_transpose(L))
+
+
 def ic_residual_on_pattern(a: CsrMatrix, f: IcFactor, kernels=None):
     """src/precond.py:203-224 (verifier; native llt_on_pattern)."""
     low_a = _strict_tri(a, upper=False)
