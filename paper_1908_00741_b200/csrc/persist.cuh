@@ -24,6 +24,16 @@
 
 #include "sweep_lean.cuh"
 
+#ifndef TB_SMALL_DEPTH
+#define TB_SMALL_DEPTH 2
+#endif
+#ifndef TB_HEAVY_DEPTH
+#define TB_HEAVY_DEPTH 2
+#endif
+#ifndef TB_HEAVY_GA
+#define TB_HEAVY_GA 0
+#endif
+
 namespace persist {
 
 constexpr int kThreads = 256;
@@ -225,17 +235,22 @@ __device__ __forceinline__ double sweep_pair_dataflow(const Params &P, const dou
   const int n = P.n_lvl1;
   double dot = 0.0;
   // blocks whose slices hold <= 2 slots (e.g. the first color of the forward
-  // sweep: in-block entries only) run the short KC = 2 chain
+  // sweep: in-block entries only) run the short KC = 2 chain, with a deeper
+  // operand ring (TB_SMALL_DEPTH) since their steps are short
   constexpr int KS = KC < 2 ? KC : 2;
+  constexpr int SD = TB_SMALL_DEPTH;
+  constexpr int HD = TB_HEAVY_DEPTH;
+  constexpr bool HG = TB_HEAVY_GA != 0;
   for (int it = gw; it < 2 * n; it += W) {
     if (it < n) {  // forward item: level-1 block k = it
       const int k = it;
       wait_flags(P, P.fflag, P.fdep, P.fdep_ptr[k], P.fdep_ptr[k + 1], epoch);
       if (P.small[k] & 1)
-        sweep_lean::lane_chain<true, KS, 32, true>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d, src,
-                                                   mid, 32, P.b_s, k, lane, ys, offs, lens);
+        sweep_lean::lane_chain<true, KS, 32, true, SD>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d,
+                                                       src, mid, 32, P.b_s, k, lane, ys, offs,
+                                                       lens);
       else
-        sweep_lean::lane_chain<true, KC, 32, true>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d, src,
+        sweep_lean::lane_chain<true, KC, 32, true, HD, HG>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d, src,
                                                    mid, 32, P.b_s, k, lane, ys, offs, lens);
       __syncwarp();
       if (lane == 0) st_release(P.fflag + k, epoch);
@@ -244,11 +259,11 @@ __device__ __forceinline__ double sweep_pair_dataflow(const Params &P, const dou
       // deps: own rows' rhs (= forward result of block k) + later-color blocks
       wait_flags(P, P.bflag, P.bdep, P.bdep_ptr[k], P.bdep_ptr[k + 1], epoch, P.fflag + k);
       if (P.small[k] & 2)
-        sweep_lean::lane_chain<false, KS, 32, true>(P.Usp, P.Usl, P.Ucol, P.Uval, P.inv_d,
-                                                    mid, dst, 32, P.b_s, k, lane, ys, offs,
-                                                    lens, dotv, &dot);
+        sweep_lean::lane_chain<false, KS, 32, true, SD>(P.Usp, P.Usl, P.Ucol, P.Uval,
+                                                        P.inv_d, mid, dst, 32, P.b_s, k, lane,
+                                                        ys, offs, lens, dotv, &dot);
       else
-        sweep_lean::lane_chain<false, KC, 32, true>(P.Usp, P.Usl, P.Ucol, P.Uval, P.inv_d,
+        sweep_lean::lane_chain<false, KC, 32, true, HD, HG>(P.Usp, P.Usl, P.Ucol, P.Uval, P.inv_d,
                                                     mid, dst, 32, P.b_s, k, lane, ys, offs,
                                                     lens, dotv, &dot);
       __syncwarp();
