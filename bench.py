@@ -287,7 +287,11 @@ def run_ours(args, rank, world, local_rank):
     pinfo = plan.persistent()
     if pinfo["precond"]:
         # the timed step is ONE persistent launch (both sweeps, all phases)
-        kernel_name = (f"pcg_persistent mode=precond (cooperative, grid {pinfo['grid']} "
+        kernel_name = (f"pcg_persistent<KC,dataflow> mode=precond (cooperative grid "
+                       f"{pinfo['grid']} CTAs, per-level-1-block completion flags, no grid "
+                       f"barrier)"
+                       if w == 32 else
+                       f"pcg_persistent mode=precond (cooperative, grid {pinfo['grid']} "
                        f"CTAs, {2 * hl.n_c - 1} in-kernel grid barriers)")
         tot_b = step_bytes * args.steps
         tot_ms = dev_ms

@@ -538,6 +538,26 @@ __global__ void __launch_bounds__(persist::kThreads, TB_PMINB)
   }
 }
 
+// Preconditioner-only dataflow launch (mode 0, w == 32).  No grid barrier
+// inside (persist.cuh: sweep_pair_dataflow), so it does not share the PCG
+// kernel's register budget: built for TB_PRE_MINB CTAs per SM, which raises
+// the number of lane chains in flight per SM.  Launched cooperatively so the
+// whole grid is co-resident (the flag waits assume every item's warp runs).
+#ifndef TB_PRE_MINB
+#define TB_PRE_MINB 4
+#endif
+template <int KC>
+__global__ void __launch_bounds__(persist::kThreads, TB_PRE_MINB)
+    precond_dataflow(const __grid_constant__ persist::Params P) {
+  extern __shared__ __align__(16) double psm[];
+  const int T = blockDim.x, b_s = P.b_s;
+  double *ys = psm;
+  int *offs = (int *)(ys + (size_t)b_s * T);
+  int *lens = offs + (size_t)b_s * T;
+  persist::sweep_pair_dataflow<KC>(P, P.pre_src, P.y, P.pre_dst, P.epoch, nullptr, ys, offs,
+                                   lens);
+}
+
 // ------------------------------------------------------------ helpers
 inline unsigned grid_for(long long n, int per_block = kBlock) {
   long long g = (n + per_block - 1) / per_block;
@@ -766,6 +786,8 @@ struct tb_plan {
   unsigned epoch = 1;
   // TMA-staged SpMV (spmv_tma.cuh): 0 slices per chunk = not configured
   int spmv_S = 0, spmv_cap = 0, spmv_D = 0, spmv_grid = 0;
+  // precond-only dataflow kernel (0 = use pcg_persistent mode 0)
+  int pre_grid = 0;
 };
 
 namespace {
@@ -1278,6 +1300,16 @@ PersistFn persist_fn(int kc, bool flow) {
   }
 }
 
+using PreFn = void (*)(persist::Params);
+PreFn pre_fn(int kc) {
+  switch (kc) {
+    case 2: return precond_dataflow<2>;
+    case 4: return precond_dataflow<4>;
+    case 6: return precond_dataflow<6>;
+    default: return precond_dataflow<8>;
+  }
+}
+
 // Decide whether the persistent kernel applies and size its cooperative grid.
 int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   pl->persist_ok = false;
@@ -1376,6 +1408,18 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
       CU(cudaMemset(pl->flags, 0, sizeof(unsigned) * 2 * nl));
       pl->n_lvl1_flow = nl;
       pl->epoch = 1;
+      // the precond-only kernel: its own occupancy (fewer registers)
+      // off by default: measured slower (spills at 64 / 85 registers beat
+      // the extra warps; profiles/README.md) -- TB_PRE_CTAS=n enables it
+      const int cap = env_int("TB_PRE_CTAS", 0);
+      if (cap > 0) {
+        PreFn pf = pre_fn(kc);
+        CU(cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+        int ps = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, pf, (int)T, smem));
+        if (ps > cap) ps = cap;
+        pl->pre_grid = ps > 0 ? ps * pl->num_sms : 0;
+      }
     }
   }
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
@@ -1448,6 +1492,11 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.state = pl->st;
   P.watchdog = 4000000000LL;  // ~2 s at 1.9 GHz per barrier wait
   void *args[] = {&P};
+  if (mode == 0 && P.n_lvl1 > 0 && pl->pre_grid > 0) {
+    CU(cudaLaunchCooperativeKernel((const void *)pre_fn(pl->persist_kc), dim3(pl->pre_grid),
+                                   dim3(persist::kThreads), args, pl->persist_smem, s));
+    return TB_OK;
+  }
   CU(cudaLaunchCooperativeKernel((const void *)persist_fn(pl->persist_kc, P.n_lvl1 > 0),
                                  dim3(pl->persist_grid), dim3(persist::kThreads), args,
                                  pl->persist_smem, s));
@@ -1715,7 +1764,7 @@ extern "C" int tb_plan_persistent(const tb_plan *pl, int32_t *precond, int32_t *
   if (!pl) return fail(TB_EINVAL, "null plan");
   *precond = pl->persist_ok;
   *pcg = pl->persist_ok && pl->persist_pcg_ok;
-  *grid = pl->persist_grid;
+  *grid = pl->pre_grid > 0 && pl->n_lvl1_flow > 0 ? pl->pre_grid : pl->persist_grid;
   return TB_OK;
 }
 

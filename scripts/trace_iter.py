@@ -12,9 +12,13 @@ import torch
 import paper_1908_00741_b200 as P
 from paper_1908_00741_b200 import _lib, problems, solver
 
-cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-label, gen, bs, w = problems.CONFIGS[cfg_id]
-a = gen()
+arg = sys.argv[1] if len(sys.argv) > 1 else "2"
+if arg.startswith("c5:"):   # config 5 family at a given grid size
+    label, bs, w = f"aniso7_{arg[3:]}^3", 16, 32
+    a = problems.lap7(int(arg[3:]), 1.0, 1.0, 1e-3)
+else:
+    label, gen, bs, w = problems.CONFIGS[int(arg)]
+    a = gen()
 xs, b = problems.rhs(a)
 cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
 s = solver.prepare(a, b, cfg)
