@@ -139,6 +139,21 @@ int tb_level_schedule(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
 int tb_spmv_csr_host(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
                      const double *vals, const double *x, double *out);
 
+/* MatrixMarket ingestion (src/io.py:70-163), byte scanning only; the
+ * caller validates banner / size line / bounds / symmetry / duplicates.
+ * tb_mm_locate: the size line (1-based number, byte range) and where the
+ * entry lines start.  tb_mm_entries: parse up to `cap` entry lines into
+ * rows / cols (1-based as written) / vals with their line numbers; *found
+ * counts all entry lines, *kth_line = line of entry number `cap` (the
+ * first surplus) or 0; first malformed line: *err_kind 1 = not three fields,
+ * 2 = bad index, 3 = non-real value, its line and the offending bytes. */
+int tb_mm_locate(const char *buf, int64_t len, int64_t *size_line, int64_t *size_b,
+                 int64_t *size_e, int64_t *body_pos, int64_t *lines);
+int tb_mm_entries(const char *buf, int64_t len, int64_t body_pos, int64_t first_line,
+                  int64_t cap, int64_t *rows, int64_t *cols, double *vals, int64_t *linenos,
+                  int64_t *found, int64_t *kth_line, int32_t *err_kind, int64_t *err_line,
+                  int64_t *err_b, int64_t *err_e);
+
 /* =========================================================================
  * Device operators on caller-owned device buffers (e.g. torch.cuda tensors
  * passed as data_ptr()).  `stream` is a cudaStream_t (NULL = legacy default).

@@ -109,6 +109,9 @@ _SIGS = {
     "tb_dev_dot": [i64, vp, vp, vp, i32, vp, vp],
     "tb_dev_cg_xr": [i64, vp, i32, i32, vp, vp, vp, vp, i32, vp, vp],
     "tb_dev_cg_p": [i64, vp, i32, i32, vp, vp, vp],
+    "tb_mm_locate": [vp, i64, P_i64, P_i64, P_i64, P_i64, P_i64],
+    "tb_mm_entries": [vp, i64, i64, i64, i64, vp, vp, vp, vp, P_i64, P_i64,
+                      C.POINTER(i32), P_i64, P_i64, P_i64],
     "tb_dev_ic0_hbmc": [i64, vp, vp, vp, vp, vp, vp, i64, i64, i64, vp, vp, P_i64, P_dbl, vp],
 }
 
