@@ -56,6 +56,7 @@ namespace {
 
 constexpr int kBlock = 256;        // threads per CTA for streaming kernels
 constexpr int kMaxPartials = 8192; // upper bound on CTAs of a reducing kernel
+constexpr int kSplitN = 0;  // tb_pcg split path from this size on (A/B: faster at config 2 and 5)
 
 // ------------------------------------------------------------ reductions
 // Deterministic CTA sum: warp shuffle tree, then warp 0 over the warp sums.
@@ -279,6 +280,29 @@ __global__ void __launch_bounds__(kBlock)
       }
       st->alpha = st->rz / pap;
     });
+}
+
+// TMA-staged SpMV (spmv_tma.cuh) with the fused p . Ap and alpha epilogue
+// of spmv_sell<true>: same grid_reduce, same state updates.
+__global__ void __launch_bounds__(spmv_tma::kThreads, 2)
+    spmv_tma_dot(const __grid_constant__ spmv_tma::Params p, double *partials, PcgState *st) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  if (st->done) return;
+  spmv_tma::init_bars(p, smem);
+  unsigned phase = 0;
+  const double part = spmv_tma::run<true>(p, smem, phase);
+  grid_reduce(part, partials, &st->counter[0], [st](double pap) {
+    const long long j = st->iter + 1;
+    st->pap = pap;
+    if (pap <= 0.0) {  // src/solver.py:176-177
+      st->status = TB_ECG_BREAKDOWN;
+      st->bd_iter = j;
+      st->bd_val = pap;
+      stop_loop(st);
+      return;
+    }
+    st->alpha = st->rz / pap;
+  });
 }
 
 // ------------------------------------------------------------ CG vectors
@@ -788,6 +812,9 @@ struct tb_plan {
   int spmv_S = 0, spmv_cap = 0, spmv_D = 0, spmv_grid = 0;
   // precond-only dataflow kernel (0 = use pcg_persistent mode 0)
   int pre_grid = 0;
+  // tb_pcg as a host-polled kernel sequence with the TMA SpMV and one
+  // persistent dataflow precond launch per iteration (large systems)
+  bool split_pcg = false;
 };
 
 namespace {
@@ -1148,7 +1175,7 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
   if (n <= 0) return TB_OK;
   if (pl->spmv_format == TB_SPMV_NONE)
     return fail(TB_EINVAL, "plan has no matrix A (preconditioner-only plan)");
-  if (pl->spmv_format == TB_SPMV_SELL && !dot && pl->spmv_S > 0) {
+  if (pl->spmv_format == TB_SPMV_SELL && pl->spmv_S > 0) {
     spmv_tma::Params P;
     P.n_slices = pl->A.n_slices;
     P.slice_ptr = pl->A.slice_ptr;
@@ -1161,8 +1188,12 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
     P.cap = pl->spmv_cap;
     P.D = pl->spmv_D;
     P.n_chunks = (pl->A.n_slices + P.S - 1) / P.S;
-    spmv_tma::spmv_kernel<<<pl->spmv_grid, spmv_tma::kThreads,
-                            spmv_tma::smem_bytes(P.cap, P.D), s>>>(P);
+    if (dot)
+      spmv_tma_dot<<<pl->spmv_grid, spmv_tma::kThreads, spmv_tma::smem_bytes(P.cap, P.D), s>>>(
+          P, pl->partials, pl->st);
+    else
+      spmv_tma::spmv_kernel<<<pl->spmv_grid, spmv_tma::kThreads,
+                              spmv_tma::smem_bytes(P.cap, P.D), s>>>(P);
   } else if (pl->spmv_format == TB_SPMV_SELL) {
     if (dot)
       (pl->A.paired ? spmv_sell<true, true> : spmv_sell<true, false>)
@@ -1188,6 +1219,23 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
 }
 
 // One CG iteration (src/solver.py:174-193) as a kernel sequence.
+int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, const double *b,
+                      double *x, cudaStream_t s, long long applications);
+
+// z = M r inside a kernel-sequence iteration: the per-color phase kernels,
+// or (split mode, host-polled loop only: the launch takes a fresh epoch from
+// the host) one persistent dataflow launch.
+int launch_precond_step(tb_plan *pl, cudaStream_t s, long long *nl) {
+  int rc;
+  if (pl->split_pcg) {
+    if ((rc = launch_persistent(pl, 0, pl->r, pl->z, nullptr, nullptr, s, 1))) return rc;
+    ++*nl;
+    return TB_OK;
+  }
+  if ((rc = launch_forward(pl, pl->r, pl->y, s, pl->st, nl))) return rc;
+  return launch_backward(pl, pl->y, pl->z, s, pl->st, nl);
+}
+
 int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   const long long n = pl->n;
   const unsigned rg = reduce_grid(n);
@@ -1196,8 +1244,7 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   cg_update_xr<<<rg, kBlock, 0, s>>>(n, pl->p, pl->ap, x, pl->r, pl->partials,
                                      pl->st, pl->hist);
   ++*nl;
-  if ((rc = launch_forward(pl, pl->r, pl->y, s, pl->st, nl))) return rc;
-  if ((rc = launch_backward(pl, pl->y, pl->z, s, pl->st, nl))) return rc;
+  if ((rc = launch_precond_step(pl, s, nl))) return rc;
   cg_rz<false><<<rg, kBlock, 0, s>>>(n, pl->r, pl->z, pl->p, pl->partials, pl->st);
   cg_update_p<<<reduce_grid(n), kBlock, 0, s>>>(n, pl->z, pl->p, pl->st);
   *nl += 2;
@@ -1212,8 +1259,7 @@ int launch_prologue(tb_plan *pl, const double *b, double *x, cudaStream_t s,
   int rc;
   cg_init<<<rg, kBlock, 0, s>>>(n, b, x, pl->r, pl->partials, pl->st, pl->hist);
   ++*nl;
-  if ((rc = launch_forward(pl, pl->r, pl->y, s, pl->st, nl))) return rc;
-  if ((rc = launch_backward(pl, pl->y, pl->z, s, pl->st, nl))) return rc;
+  if ((rc = launch_precond_step(pl, s, nl))) return rc;
   cg_rz<true><<<rg, kBlock, 0, s>>>(n, pl->r, pl->z, pl->p, pl->partials, pl->st);
   ++*nl;
   CU(cudaGetLastError());
@@ -1433,7 +1479,7 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
 // mode 0: z = M r (src -> dst); mode 1: whole PCG (b, x; state preset).
 // `applications` = preconditioner applications the launch may perform (epochs).
 int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, const double *b,
-                      double *x, cudaStream_t s, long long applications = 1) {
+                      double *x, cudaStream_t s, long long applications) {
   persist::Params P;
   memset(&P, 0, sizeof(P));
   if (pl->n_lvl1_flow > 0) {
@@ -1510,10 +1556,20 @@ int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
   pl->spmv_S = 0;
   if (env_int("TB_SPMV_TMA", 1) == 0 || h.width != 32 || pl->A.paired || h.n_slices <= 0)
     return TB_OK;
-  if (h.slice_ptr[h.n_slices] > 0x7fffffffLL) return TB_OK;
-  const int D = env_int("TB_SPMV_D", 4);
-  const size_t budget = (size_t)env_int("TB_SPMV_KB", 100) * 1024;
-  for (int S = env_int("TB_SPMV_S", 8); S >= 1; S /= 2) {
+  const long long slots = h.slice_ptr[h.n_slices];
+  if (slots > 0x7fffffffLL) return TB_OK;
+  // Heavily padded SELL (the kNN graph, 1.35x): the stage would carry the
+  // padding and the scattered gathers dominate -- the thread-per-row kernel
+  // measured faster there (profiles/README.md).
+  long long pad = 0;
+  for (long long s = 0; s < h.n_slices; ++s) {
+    const long long off = h.slice_ptr[s];
+    for (long long q = off; q < off + (long long)h.slice_len[s] * 32; ++q)
+      pad += h.vals[q] == 0.0 && h.col_idx[q] == s * 32 + (q - off) % 32;
+  }
+  if (env_int("TB_SPMV_S", 0) == 0 && slots > 0 && (double)slots > 1.2 * (double)(slots - pad))
+    return TB_OK;
+  auto cap_of = [&](int S) {
     long long cap = 0;
     for (long long s0 = 0; s0 < h.n_slices; s0 += S) {
       const long long s1 = s0 + S < h.n_slices ? s0 + S : h.n_slices;
@@ -1521,27 +1577,46 @@ int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
       cap = c > cap ? c : cap;
     }
     cap = (cap + 31) / 32 * 32;
-    if (cap < 32) cap = 32;
-    const size_t sm = spmv_tma::smem_bytes((int)cap, D);
-    if (sm > budget) continue;
-    // S < 8 leaves warps of the CTA without a slice (long rows, e.g. the
-    // 27-point and kNN configs): the thread-per-row kernel is faster there
-    if (S < spmv_tma::kWarps && env_int("TB_SPMV_S", 0) == 0) return TB_OK;
+    return cap < 32 ? 32LL : cap;
+  };
+  // candidates (slices per chunk, stages, smem budget KB) in order of
+  // preference, from the A/B in profiles/README.md: 16 slices (two per warp,
+  // 16 gathers in flight per lane) x 2 stages at 2 CTAs/SM for short rows;
+  // one 16-slice stage at 1 CTA/SM for long rows (27-point)
+  struct Cand { int S, D, kb; };
+  Cand cands[3] = {{16, 2, 100}, {16, 1, 220}, {0, 0, 0}};
+  if (env_int("TB_SPMV_S", 0) > 0)
+    cands[0] = {env_int("TB_SPMV_S", 16), env_int("TB_SPMV_D", 2), env_int("TB_SPMV_KB", 100)},
+    cands[1] = {0, 0, 0};
+  int optin = 0;
+  CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
+  for (const Cand &c : cands) {
+    if (c.S <= 0) break;
+    const long long cap = cap_of(c.S);
+    const size_t sm = spmv_tma::smem_bytes((int)cap, c.D);
+    if (sm > (size_t)c.kb * 1024 || sm + 1024 > (size_t)optin) continue;
     // the attribute is per function, shared by every plan: set it to the
     // device maximum once instead of this plan's size
-    int optin = 0;
-    CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
     CU(cudaFuncSetAttribute(spmv_tma::spmv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             optin));
-    int per_sm = 0;
+    {  // dynamic + static (grid_reduce's) shared memory must fit the opt-in maximum
+      cudaFuncAttributes fa;
+      CU(cudaFuncGetAttributes(&fa, spmv_tma_dot));
+      CU(cudaFuncSetAttribute(spmv_tma_dot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - (int)fa.sharedSizeBytes));
+    }
+    int per_sm = 0, per_sm_dot = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_tma::spmv_kernel,
                                                      spmv_tma::kThreads, sm));
-    if (per_sm < 1) return TB_OK;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_dot, spmv_tma_dot,
+                                                     spmv_tma::kThreads, sm));
+    per_sm = per_sm_dot < per_sm ? per_sm_dot : per_sm;
+    if (per_sm < 1) continue;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
-    pl->spmv_S = S;
+    pl->spmv_S = c.S;
     pl->spmv_cap = (int)cap;
-    pl->spmv_D = D;
+    pl->spmv_D = c.D;
     pl->spmv_grid = per_sm * nsm;
     return TB_OK;
   }
@@ -1727,7 +1802,7 @@ extern "C" int tb_plan_precond(tb_plan *pl, const double *r, double *z, void *st
   if (!pl) return fail(TB_EINVAL, "null plan");
   CU(cudaSetDevice(pl->device));
   if (pl->persist_ok)  // one cooperative launch for all color phases of both sweeps
-    return launch_persistent(pl, 0, r, z, nullptr, nullptr, (cudaStream_t)stream);
+    return launch_persistent(pl, 0, r, z, nullptr, nullptr, (cudaStream_t)stream, 1);
   long long nl = 0;
   int rc = launch_forward(pl, r, pl->y, (cudaStream_t)stream, nullptr, &nl);
   if (rc) return rc;
@@ -1822,6 +1897,19 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
   CU(cudaMemcpy(pl->st, &hs, sizeof(PcgState), cudaMemcpyHostToDevice));
   int rc;
   long long polled_launches = 0, polls = 0;
+  // Split path (large systems): kernel sequence with the TMA SpMV and one
+  // persistent dataflow precond launch per iteration, host polling every
+  // check_every iterations (each launch takes a fresh flag epoch).
+  // TB_PCG_SPLIT=1/0 forces it on/off; default: n >= TB_PCG_SPLIT_N.
+  {
+    const int se = env_int("TB_PCG_SPLIT", -1);
+    const long long sn = (long long)env_int("TB_PCG_SPLIT_N", kSplitN);
+    // default only with the double-buffered TMA SpMV (short rows: configs
+    // 1, 2, 5); long rows (27-point) measured faster in the single launch
+    pl->split_pcg = pl->persist_ok && pl->n_lvl1_flow > 0 && pl->spmv_S > 0 &&
+                    (se == 1 || (se < 0 && pl->n >= sn && pl->spmv_D >= 2));
+    if (pl->split_pcg && check_every <= 0) check_every = env_int("TB_PCG_SPLIT_POLL", 4);
+  }
   const bool persistent = check_every <= 0 && pl->persist_ok && pl->persist_pcg_ok;
   if (persistent) {
     if ((rc = sync_in(pl, stream))) return rc;
@@ -1855,6 +1943,7 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
     CU(cudaMemcpyAsync(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost, pl->stream));
     CU(cudaStreamSynchronize(pl->stream));
   }
+  pl->split_pcg = false;
   if ((rc = sync_out(pl, stream))) return rc;
   const long long iters = hs.iter;
   CU(cudaMemcpy(history_host, pl->hist, sizeof(double) * (size_t)(iters + 1),

@@ -61,7 +61,35 @@ __device__ __forceinline__ void issue(const Params &p, long long q, unsigned cha
   }
 }
 
-// Rows of chunk q from stage memory; returns the DOT partial.
+// One slice row (lane) of the stage: acc = 0; acc = acc + v * x[col].
+// Two slices per call (the second may be absent: len1 = -1) so a lane keeps
+// 2 * kG gathers in flight.
+__device__ __forceinline__ void rows2(const double *sv, const int *sc, int off0, int len0,
+                                      int off1, int len1, const double *x, double &acc0,
+                                      double &acc1) {
+  const int lm = len0 > len1 ? len0 : len1;
+  for (int t0 = 0; t0 < lm; t0 += kG) {
+    double v0[kG], x0[kG], v1[kG], x1[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const bool i0 = t0 + u < len0, i1 = t0 + u < len1;
+      const int c0 = i0 ? sc[off0 + (t0 + u) * 32] : 0;
+      const int c1 = i1 ? sc[off1 + (t0 + u) * 32] : 0;
+      v0[u] = i0 ? sv[off0 + (t0 + u) * 32] : 0.0;
+      v1[u] = i1 ? sv[off1 + (t0 + u) * 32] : 0.0;
+      x0[u] = i0 ? __ldcg(x + c0) : 0.0;
+      x1[u] = i1 ? __ldcg(x + c1) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      if (t0 + u < len0) acc0 = __dadd_rn(acc0, __dmul_rn(v0[u], x0[u]));
+      if (t0 + u < len1) acc1 = __dadd_rn(acc1, __dmul_rn(v1[u], x1[u]));
+    }
+  }
+}
+
+// Rows of chunk q from stage memory; returns the DOT partial.  Warp w takes
+// slices w, w + kWarps, ... of the chunk, two at a time.
 template <bool DOT>
 __device__ __forceinline__ double compute(const Params &p, long long q,
                                           const unsigned char *stage, int cap) {
@@ -72,26 +100,22 @@ __device__ __forceinline__ double compute(const Params &p, long long q,
   const long long s1 = s0 + p.S < p.n_slices ? s0 + p.S : p.n_slices;
   const long long base = p.slice_ptr[s0];
   double part = 0.0;
-  for (long long s = s0 + warp; s < s1; s += kWarps) {
-    const int off = (int)(p.slice_ptr[s] - base) + lane;
-    const int len = p.slice_len[s];
-    const long long row = s * 32 + lane;
-    double acc = 0.0;
-    for (int t0 = 0; t0 < len; t0 += kG) {
-      double v[kG], xv[kG];
-#pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        const bool in = t0 + u < len;
-        const int c = in ? sc[off + (t0 + u) * 32] : 0;
-        v[u] = in ? sv[off + (t0 + u) * 32] : 0.0;
-        xv[u] = in ? __ldcg(p.x + c) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kG; ++u)
-        if (t0 + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+  for (long long s = s0 + warp; s < s1; s += 2 * kWarps) {
+    const long long t = s + kWarps;
+    const bool two = t < s1;
+    const int off0 = (int)(p.slice_ptr[s] - base) + lane, len0 = p.slice_len[s];
+    const int off1 = two ? (int)(p.slice_ptr[t] - base) + lane : 0;
+    const int len1 = two ? p.slice_len[t] : -1;
+    double acc0 = 0.0, acc1 = 0.0;
+    rows2(sv, sc, off0, len0, off1, len1, p.x, acc0, acc1);
+    const long long r0 = s * 32 + lane;
+    p.out[r0] = acc0;
+    if (DOT) part += __ldcg(p.x + r0) * acc0;
+    if (two) {
+      const long long r1 = t * 32 + lane;
+      p.out[r1] = acc1;
+      if (DOT) part += __ldcg(p.x + r1) * acc1;
     }
-    p.out[row] = acc;
-    if (DOT) part += __ldcg(p.x + row) * acc;
   }
   return part;
 }

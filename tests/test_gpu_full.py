@@ -228,3 +228,29 @@ def test_plan_spmv_bitwise(P, name):
     ref = g["spmv_sell"]
     assert np.array_equal(y.cpu().numpy()[: ref.shape[0]], ref)
     st.plan.close()
+
+
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32", "aniso12_b16_w32",
+                                  "s27_10_b8_w32"])
+def test_split_pcg_path(P, name, monkeypatch):
+    """The split PCG path (TMA SpMV + p.Ap, one persistent dataflow precond
+    launch per iteration, host-polled) against the reference's golden run."""
+    monkeypatch.setenv("TB_PCG_SPLIT", "1")
+    g = load_golden(name)
+    a, bs, w, _ = golden_matrix(name)
+    from paper_1908_00741_b200 import problems
+    _, b = problems.rhs(a)
+    x, rep = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell"))
+    assert abs(rep.iterations - int(g["pcg_hbmc_iters"])) <= 1
+    assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
+
+
+def test_split_pcg_full_config2(P, monkeypatch):
+    from paper_1908_00741_b200 import problems
+    monkeypatch.setenv("TB_PCG_SPLIT", "1")
+    dg = _digest(2)
+    label, gen, bs, w = problems.CONFIGS[2]
+    a = gen()
+    _, b = problems.rhs(a)
+    x, rep = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell"))
+    _check_against_digest(rep, x, dg)
