@@ -28,7 +28,10 @@ cpu_baseline = the CPU oracle port of the reference path (oracle/), all host
 
 N > 1 (torchrun, one rank per GPU, NCCL): the row-partitioned solve of
 SURVEY 8(e) -- every color's level-1 blocks split over the ranks, one halo
-exchange (NCCL P2P over NVLink) after every color phase, CG dots all-reduced.
+exchange after every color phase (default: the owner's kernel stores the
+halo entries straight into the peers' vectors over NVLink through CUDA IPC
+mappings and releases a per-sender flag; `--transport nccl`: NCCL
+send/recv), CG dots all-reduced with NCCL.
 The problem is fixed as N grows (scaling "strong"); value = the whole
 system's algorithmic sweep bytes / max-over-ranks device time.
 `--mode replicas` instead runs N independent replicas (scaling "weak").
@@ -486,7 +489,7 @@ def run_partitioned(args, rank, world, local_rank):
     setup = solver.prepare(a, b, cfg)
     part = D.partition_setup(setup, world, ranks=[rank])[0]
     ops = D.CudaRankOps(part)
-    drv = D.DistHbmc([part], [ops])
+    drv = D.DistHbmc([part], [ops], transport=args.transport)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     hl = setup.layout
@@ -505,7 +508,7 @@ def run_partitioned(args, rank, world, local_rank):
 
     r_glob = np.random.default_rng(0).standard_normal(hl.n_pad)
     r = [ops.from_host(np.concatenate([r_glob[part.rows], np.zeros(part.n_halo)]))]
-    y, z = [ops.vec()], [ops.vec()]
+    y, z = [drv.ext_vec(0, "y")], [drv.ext_vec(0, "z")]
     for _ in range(args.warmup):
         flush()
         drv.precond(r, y, z)
@@ -561,7 +564,8 @@ def run_partitioned(args, rank, world, local_rank):
                        "N": a.n, "n_pad": hl.n_pad, "nnz_L": nnz_l, "n_c": hl.n_c,
                        "bytes_per_step": step_bytes,
                        "l2": "flushed before every timed step (256 MiB read)",
-                       "parallelism": f"row-partitioned x{world} (per-color halo over NCCL P2P)",
+                       "parallelism": f"row-partitioned x{world} (per-color halo exchange: "
+                                      f"{'NVLink peer stores + flags' if args.transport == 'p2p' else 'NCCL send/recv'})",
                        "halo_rows_rank0": part.n_halo, "rows_rank0": part.n_loc},
             "roofline": {"bound": "hbm", "kernel": "per-rank HBMC sweep phases + halo exchange",
                          "achieved": per_gpu, "peak": peak, "unit": "GB/s",
@@ -577,6 +581,7 @@ def run_partitioned(args, rank, world, local_rank):
                      "exchanges_per_precond": 2 * max(hl.n_c - 1, 0)},
         }
         print(json.dumps(line), flush=True)
+    drv.close()
     ops.close()
     dist.barrier()
 
@@ -591,6 +596,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="partitioned", choices=["partitioned", "replicas"],
                     help="N > 1: row-partitioned solve (default) or independent replicas")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="partitioned halo exchange: NVLink peer stores (default) or NCCL")
     ap.add_argument("--force-partitioned", action="store_true",
                     help="run the partitioned path even at N = 1 (code-path check)")
     ap.add_argument("--traffic", type=float, default=None,

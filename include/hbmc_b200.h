@@ -333,6 +333,23 @@ int tb_dev_cg_xr(int64_t n, double *s, int32_t num, int32_t den, const double *p
 int tb_dev_cg_p(int64_t n, const double *s, int32_t num, int32_t den, const double *z,
                 double *p, void *stream);
 
+/* NVLink P2P halo exchange (partitioned solve without NCCL on the data path).
+ * tb_p2p_alloc: device buffer (zeroed) + its CUDA IPC handle (64 bytes) for
+ * peers; tb_p2p_open / close map / unmap a peer's buffer.  tb_p2p_push:
+ * dst_remote[i] = src[idx[i]] (remote = peer-mapped), then, after all its
+ * stores, *flag_remote = epoch (release, system scope); done_ctr: one zeroed
+ * device word of the sender, private to this push.  tb_p2p_wait: block the
+ * stream until flags[q] >= epoch for q in [0, count), q != skip (acquire,
+ * system scope; traps after ~4 s instead of hanging). */
+int tb_p2p_alloc(int64_t bytes, void **ptr, void *handle64);
+int tb_p2p_free(void *ptr);
+int tb_p2p_open(const void *handle64, void **ptr);
+int tb_p2p_close(void *ptr);
+int tb_p2p_push(int64_t n, const int32_t *idx, const double *src, double *dst_remote,
+                uint32_t *flag_remote, uint32_t epoch, uint32_t *done_ctr, void *stream);
+int tb_p2p_wait(const uint32_t *flags, int32_t count, int32_t skip, uint32_t epoch,
+                void *stream);
+
 /* K/numba_backend.py:40-79 ic0_factor on the device, bitwise, for a system
  * in HBMC order (src/precond.py:179-200 with layout "hbmc"): one launch per
  * color, thread per (level-1 block, lane) walking its b_s rows.  lrp / lci /

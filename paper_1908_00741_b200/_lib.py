@@ -109,6 +109,12 @@ _SIGS = {
     "tb_dev_dot": [i64, vp, vp, vp, i32, vp, vp],
     "tb_dev_cg_xr": [i64, vp, i32, i32, vp, vp, vp, vp, i32, vp, vp],
     "tb_dev_cg_p": [i64, vp, i32, i32, vp, vp, vp],
+    "tb_p2p_alloc": [i64, C.POINTER(vp), vp],
+    "tb_p2p_free": [vp],
+    "tb_p2p_open": [vp, C.POINTER(vp)],
+    "tb_p2p_close": [vp],
+    "tb_p2p_push": [i64, vp, vp, vp, vp, C.c_uint32, vp, vp],
+    "tb_p2p_wait": [vp, i32, i32, C.c_uint32, vp],
     "tb_mm_locate": [vp, i64, P_i64, P_i64, P_i64, P_i64, P_i64],
     "tb_mm_entries": [vp, i64, i64, i64, i64, vp, vp, vp, vp, P_i64, P_i64,
                       C.POINTER(i32), P_i64, P_i64, P_i64],

@@ -21,6 +21,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "tb_internal.h"
 
 using tb::fail;
@@ -152,6 +154,107 @@ extern "C" int tb_dev_cg_p(int64_t n, const double *scal, int32_t num, int32_t d
   if (n < 0 || num < 0 || den < 0) return fail(TB_EINVAL, "dev_cg_p: bad arguments");
   if (n == 0) return TB_OK;
   p_kernel<<<grid_of(n), kT, 0, (cudaStream_t)stream>>>(n, scal, num, den, z, p);
+  CU(cudaGetLastError());
+  return TB_OK;
+}
+
+// ===================================================================== P2P
+// NVLink halo exchange without NCCL (north star: "exchanges
+// halo entries per color by NVLink P2P stores").  The sender's push kernel
+// gathers its owned entries and STORES them straight into the receiver's
+// halo slice through a peer pointer (CUDA IPC mapping of the receiver's
+// vector), then the CTA that finishes last publishes the step's epoch in the
+// receiver's flag word with a system-scope release.  The receiver runs a
+// one-thread wait kernel (system-scope acquire, watchdog) on its stream
+// before the next color phase.  Epochs only grow and every exchange step
+// writes its own halo slots (steps of one sweep cover different colors; the
+// CG all-reduces separate iterations), so one flag per (receiver, sender)
+// compared with >= is enough.
+
+namespace {
+
+__global__ void __launch_bounds__(kT) push_kernel(long long n, const int *__restrict__ idx,
+                                                  const double *__restrict__ src,
+                                                  double *dst_remote, unsigned *flag_remote,
+                                                  unsigned epoch, unsigned *done_ctr) {
+  for (long long i = (long long)blockIdx.x * kT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kT)
+    dst_remote[i] = src[idx[i]];
+  // last CTA out publishes the flag after every CTA's stores are visible
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    *done_ctr = 0;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_remote), "r"(epoch) : "memory");
+  }
+}
+
+__global__ void wait_kernel(const unsigned *flags, int count, int skip, unsigned epoch,
+                            long long watchdog) {
+  for (int q = 0; q < count; ++q) {
+    if (q == skip) continue;
+    const long long t0 = clock64();
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + q) : "memory");
+      if ((int)(v - epoch) >= 0) break;
+      if (clock64() - t0 > watchdog) __trap();
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int tb_p2p_alloc(int64_t bytes, void **ptr, void *handle64) {
+  *ptr = nullptr;
+  if (bytes <= 0) return fail(TB_EINVAL, "p2p_alloc: bytes <= 0");
+  CU(cudaMalloc(ptr, (size_t)bytes));
+  CU(cudaMemset(*ptr, 0, (size_t)bytes));
+  if (handle64) {
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, *ptr));
+    memcpy(handle64, &h, sizeof(h) < 64 ? sizeof(h) : 64);
+  }
+  return TB_OK;
+}
+
+extern "C" int tb_p2p_free(void *ptr) {
+  if (ptr) CU(cudaFree(ptr));
+  return TB_OK;
+}
+
+extern "C" int tb_p2p_open(const void *handle64, void **ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  CU(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return TB_OK;
+}
+
+extern "C" int tb_p2p_close(void *ptr) {
+  if (ptr) CU(cudaIpcCloseMemHandle(ptr));
+  return TB_OK;
+}
+
+extern "C" int tb_p2p_push(int64_t n, const int32_t *idx, const double *src, double *dst_remote,
+                           uint32_t *flag_remote, uint32_t epoch, uint32_t *done_ctr,
+                           void *stream) {
+  if (n < 0 || !flag_remote || !done_ctr) return fail(TB_EINVAL, "p2p_push: bad arguments");
+  int g = grid_of(n);
+  if (g > 264) g = 264;
+  push_kernel<<<g, kT, 0, (cudaStream_t)stream>>>(n, idx, src, dst_remote, flag_remote, epoch,
+                                                  done_ctr);
+  CU(cudaGetLastError());
+  return TB_OK;
+}
+
+extern "C" int tb_p2p_wait(const uint32_t *flags, int32_t count, int32_t skip, uint32_t epoch,
+                           void *stream) {
+  if (count <= 0) return TB_OK;
+  wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flags, count, skip, epoch, 8000000000LL);
   CU(cudaGetLastError());
   return TB_OK;
 }

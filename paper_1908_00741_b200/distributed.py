@@ -139,6 +139,121 @@ class CudaRankOps:
             self.plan.close()
 
 
+class _DevBuf:
+    """A raw device allocation viewed as a torch tensor (no copy)."""
+
+    def __init__(self, ptr, n, dtype_str, device):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": dtype_str,
+                                         "data": (ptr, False), "version": 3}
+        self.device = device
+
+
+class P2PTransport:
+    """NVLink halo exchange by peer stores (csrc/dist.cu tb_p2p_*), no NCCL
+    on the data path.
+
+    Every local rank owns peer-visible copies of the exchanged vectors
+    (y, z, p: `vec(name)`) and a flag word per sender.  Exchange step e:
+    each rank pushes every message straight into the receiver's halo slice
+    (gather + remote store in one kernel) and publishes epoch e in the
+    receiver's flag for this sender -- an empty push to the peers it sends
+    nothing to, so every receiver waits on all world - 1 flags -- then each
+    rank's stream waits (acquire, system scope) for its flags before the next
+    phase.  All ranks run the same exchange sequence, so epochs agree.
+    Remote ranks' buffers are mapped through CUDA IPC handles exchanged with
+    torch.distributed (all_gather_object); local (virtual) ranks use the
+    pointers directly.
+    """
+
+    NAMES = ("y", "z", "p")
+
+    def __init__(self, drv):
+        import ctypes as C
+        t = drv.ops[0].t
+        self.t, self.drv = t, drv
+        self.world = drv.world
+        self.epoch = 0
+        self.bufs = []          # per local rank: {name: (ptr, tensor)}
+        self.flags = []         # per local rank: (ptr, tensor uint32[world])
+        self.ctr = []           # per local rank: (ptr, tensor) push completion counter
+        dev = t.device("cuda", t.cuda.current_device())
+        mine = {}
+        for i, p in enumerate(drv.parts):
+            entry, handles = {}, {}
+            for name in self.NAMES + ("flags", "ctr"):
+                n = p.n_ext if name in self.NAMES else (self.world if name == "flags" else 1)
+                nbytes = 8 * max(n, 1) if name in self.NAMES else 4 * max(n, 1)
+                ptr = C.c_void_p()
+                h = (C.c_char * 64)()
+                _lib.check(_lib.LIB.tb_p2p_alloc(nbytes, C.byref(ptr), h))
+                ts = "<f8" if name in self.NAMES else "<u4"
+                tens = t.as_tensor(_DevBuf(ptr.value, max(n, 1), ts, dev), device=dev)
+                entry[name] = (ptr.value, tens)
+                handles[name] = bytes(h)
+            self.bufs.append(entry)
+            mine[p.rank] = handles
+        # peer pointers: rank -> name -> device pointer
+        self.peer = {p.rank: {k: v[0] for k, v in self.bufs[i].items()}
+                     for i, p in enumerate(drv.parts)}
+        self.opened = []
+        if drv.dist is not None:
+            allh = [None] * self.world
+            drv.dist.all_gather_object(allh, mine, group=drv.group)
+            for hmap in allh:
+                for rank, handles in hmap.items():
+                    if rank in self.peer:
+                        continue
+                    self.peer[rank] = {}
+                    for name, h in handles.items():
+                        if name == "ctr":
+                            continue
+                        ptr = C.c_void_p()
+                        _lib.check(_lib.LIB.tb_p2p_open(h, C.byref(ptr)))
+                        self.peer[rank][name] = ptr.value
+                        self.opened.append(ptr.value)
+        self.idx = {}
+
+    def vec(self, i, name):
+        return self.bufs[i][name][1][: self.drv.parts[i].n_ext]
+
+    def exchange(self, kind, c, name, exs):
+        from . import device as D
+        self.epoch = (self.epoch + 1) & 0x7fffffff
+        st = D.current_stream()
+        for i, (p, ex) in enumerate(zip(self.drv.parts, exs)):
+            src = self.bufs[i][name][0]
+            ctr = self.bufs[i]["ctr"][0]
+            key = (kind, c, i)
+            idx = self.idx.get(key)
+            if idx is None and ex.n_send:
+                idx = self.idx[key] = self.t.from_numpy(ex.send_idx).cuda()
+            sent = set()
+            for m in ex.sends:
+                sent.add(m.peer)
+                _lib.check(_lib.LIB.tb_p2p_push(
+                    m.count, idx.data_ptr() + 4 * m.offset, src,
+                    self.peer[m.peer][name] + 8 * m.remote_offset,
+                    self.peer[m.peer]["flags"] + 4 * p.rank, self.epoch, ctr, st))
+                self.drv.bytes_sent += 8 * m.count
+            for d in range(self.world):   # flag-only pushes keep every waiter uniform
+                if d != p.rank and d not in sent:
+                    _lib.check(_lib.LIB.tb_p2p_push(0, None, src, None,
+                                                    self.peer[d]["flags"] + 4 * p.rank,
+                                                    self.epoch, ctr, st))
+        for i, p in enumerate(self.drv.parts):
+            _lib.check(_lib.LIB.tb_p2p_wait(self.bufs[i]["flags"][0], self.world, p.rank,
+                                            self.epoch, st))
+
+    def close(self):
+        for ptr in self.opened:
+            _lib.LIB.tb_p2p_close(ptr)
+        self.opened = []
+        for entry in self.bufs:
+            for ptr, _ in entry.values():
+                _lib.LIB.tb_p2p_free(ptr)
+        self.bufs = []
+
+
 class DistHbmc:
     """Lockstep driver of the local ranks of this process.
 
@@ -146,7 +261,7 @@ class DistHbmc:
     per process under torch.distributed, with part.rank == dist rank).
     """
 
-    def __init__(self, parts, ops, group=None):
+    def __init__(self, parts, ops, group=None, transport="nccl"):
         self.parts = list(parts)
         self.ops = list(ops)
         self.world = self.parts[0].world
@@ -169,6 +284,7 @@ class DistHbmc:
                         self.sendbuf[(key_kind, c, i)] = self.ops[i].vec(ex.n_send)
         self.exchanges = 0
         self.bytes_sent = 0
+        self.p2p = P2PTransport(self) if transport == "p2p" else None
 
     @staticmethod
     def _ex(p, kind, c):
@@ -179,6 +295,14 @@ class DistHbmc:
         """Deliver the owners' values of `vecs` (one extended vector per local
         rank) into the peers' halo slices for exchange step (kind, c)."""
         exs = [self._ex(p, kind, c) for p in self.parts]
+        if self.p2p is not None:
+            name = self._p2p_name(vecs)
+            if kind != "spmv" and ((kind == "fwd" and c == self.n_c - 1) or
+                                   (kind == "bwd" and c == 0)):
+                return   # no exchange after the last phase of a sweep (any transport)
+            self.p2p.exchange(kind, c, name, exs)
+            self.exchanges += 1
+            return
         if all(ex.n_send == 0 and not ex.recvs for ex in exs):
             return
         for i, ex in enumerate(exs):
@@ -206,6 +330,28 @@ class DistHbmc:
             for req in self.dist.batch_isend_irecv(p2p):
                 req.wait()
         self.exchanges += 1
+
+    def _p2p_name(self, vecs):
+        # identify the buffer on a local rank that has rows (an empty rank's
+        # views are zero-length and their data pointers may coincide)
+        i = next((k for k, p in enumerate(self.parts) if p.n_ext > 0), 0)
+        ptr = vecs[i].data_ptr()
+        for name in P2PTransport.NAMES:
+            if self.p2p.vec(i, name).data_ptr() == ptr:
+                return name
+        raise ValueError("p2p exchange: vector is not a peer-visible buffer (use ext_vec)")
+
+    def ext_vec(self, i, name):
+        """Extended vector of local rank i; with the P2P transport the
+        exchanged ones (y, z, p) live in peer-visible buffers."""
+        if self.p2p is not None and name in P2PTransport.NAMES:
+            return self.p2p.vec(i, name)
+        return self.ops[i].vec()
+
+    def close(self):
+        if self.p2p is not None:
+            self.p2p.close()
+            self.p2p = None
 
     # ---------------------------------------------------------------- reductions
     def allreduce(self, scals, slots):
@@ -247,8 +393,8 @@ class DistHbmc:
         """
         R = range(len(self.parts))
         O = self.ops
-        V = lambda: [O[i].vec() for i in R]  # noqa: E731
-        x, r, y, z, p, ap = V(), V(), V(), V(), V(), V()
+        V = lambda name: [self.ext_vec(i, name) for i in R]  # noqa: E731
+        x, r, y, z, p, ap = V("x"), V("r"), V("y"), V("z"), V("p"), V("ap")
         sc = [O[i].scalars() for i in R]
         for i in R:
             O[i].fill_zero(x[i])
@@ -303,7 +449,7 @@ def partition_setup(setup, world, ranks=None):
                           sf.b_s, sf.w, world, ranks)
 
 
-def pcg_partitioned(a, b, cfg, world, matrix_name="", group=None):
+def pcg_partitioned(a, b, cfg, world, matrix_name="", group=None, transport="nccl"):
     """HBMC ICCG with the rows partitioned over `world` ranks.
 
     Without torch.distributed: all `world` ranks are driven by this process
@@ -330,7 +476,7 @@ def pcg_partitioned(a, b, cfg, world, matrix_name="", group=None):
         raise ValueError("pcg_partitioned: world != torch.distributed world size")
     parts = partition_setup(setup, world, ranks)
     ops = [CudaRankOps(p) for p in parts]
-    drv = DistHbmc(parts, ops, group)
+    drv = DistHbmc(parts, ops, group, transport=transport)
     b_loc = [ops[i].from_host(setup.b_sys[p.rows]) for i, p in enumerate(parts)]
     ops[0].t.cuda.synchronize()
     t_setup = time.perf_counter() - t0
@@ -347,6 +493,7 @@ def pcg_partitioned(a, b, cfg, world, matrix_name="", group=None):
         dist.all_reduce(xt, group=group)
         x_sys = xt.cpu().numpy()
     t_solve = time.perf_counter() - t1
+    drv.close()
     for o in ops:
         o.close()
     x_out = x_sys[setup.old_positions]

@@ -49,6 +49,7 @@ class Msg:
     peer: int
     offset: int
     count: int
+    remote_offset: int = -1   # sends: where the values land in the peer's extended vector
 
 
 @dataclass
@@ -236,7 +237,8 @@ def partition_hbmc(L, U, A, inv_d, color_lvl1_ranges, b_s, w, world, ranks=None)
                     a, b = (a, c2) if kind == "fwd" else (c0, b)
                 if b > a:
                     send_idx.append(local_of(halos[d][0][a:b]))
-                    sends.append(Msg(d, off, b - a))
+                    n_loc_d = lvl1[d].shape[0] * span
+                    sends.append(Msg(d, off, b - a, n_loc_d + a))
                     off += b - a
             for s in range(world):
                 if s == g:

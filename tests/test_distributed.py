@@ -160,6 +160,7 @@ def test_partition_structure(name, world):
                     q = parts[m.peer]
                     rm = [r for r in D.DistHbmc._ex(q, kind, c).recvs if r.peer == p.rank]
                     assert len(rm) == 1 and rm[0].count == m.count
+                    assert m.remote_offset == rm[0].offset   # P2P store target
                     sent_rows = p.rows[ex.send_idx[m.offset:m.offset + m.count]]
                     recv_rows = q.halo_rows[rm[0].offset - q.n_loc:rm[0].offset - q.n_loc + m.count]
                     assert np.array_equal(sent_rows, recv_rows)

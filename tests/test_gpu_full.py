@@ -254,3 +254,50 @@ def test_split_pcg_full_config2(P, monkeypatch):
     _, b = problems.rhs(a)
     x, rep = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell"))
     _check_against_digest(rep, x, dg)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32", "aniso12_b16_w32",
+                                  "grid32_b8_w4"])
+def test_p2p_transport_sweeps_spmv_bitwise(P, name, world):
+    """NVLink-style transport (peer stores + release/acquire flags, no NCCL)
+    with virtual ranks on one device: the pushes of every rank precede every
+    wait in stream order, so no kernel ever waits on another rank's kernel."""
+    import torch
+    from paper_1908_00741_b200 import distributed
+    g = load_golden(name)
+    a, b, cfg, st, parts, ops, _ = _parts(P, name, world)
+    drv = distributed.DistHbmc(parts, ops, transport="p2p")
+    n = st.layout.n_pad
+    r = _scatter(ops, parts, g["r"])
+    y = [drv.ext_vec(i, "y") for i in range(world)]
+    z = [drv.ext_vec(i, "z") for i in range(world)]
+    for v in y + z:
+        v.fill_(float("nan"))
+    drv.sweep(True, r, y)
+    drv.sweep(False, y, z)
+    torch.cuda.synchronize()
+    assert np.array_equal(_gather(ops, parts, y, n), g["y"])
+    assert np.array_equal(_gather(ops, parts, z, n), g["z"])
+    p = [drv.ext_vec(i, "p") for i in range(world)]
+    for i, pp in enumerate(parts):
+        p[i][: pp.n_loc].copy_(torch.from_numpy(g["spmv_x"][pp.rows]))
+    ax = [ops[i].vec() for i in range(world)]
+    drv.spmv(p, ax)
+    got = _gather(ops, parts, ax, n)
+    assert np.array_equal(got[: g["spmv_sell"].shape[0]], g["spmv_sell"])
+    assert drv.p2p.epoch == drv.exchanges
+    drv.close()
+    for o in ops:
+        o.close()
+
+
+def test_p2p_transport_pcg_full_config2(P):
+    from paper_1908_00741_b200 import distributed, problems
+    dg = _digest(2)
+    label, gen, bs, w = problems.CONFIGS[2]
+    a = gen()
+    _, b = problems.rhs(a)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    x, rep = distributed.pcg_partitioned(a, b, cfg, 2, transport="p2p")
+    _check_against_digest(rep, x, dg)
