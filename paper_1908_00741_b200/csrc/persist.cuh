@@ -33,6 +33,9 @@
 #ifndef TB_HEAVY_GA
 #define TB_HEAVY_GA 0
 #endif
+#ifndef TB_PAIR_LAST
+#define TB_PAIR_LAST 0   // A/B: no gain at config 2 or 5 (profiles/README.md)
+#endif
 
 namespace persist {
 
@@ -241,33 +244,55 @@ __device__ __forceinline__ double sweep_pair_dataflow(const Params &P, const dou
   constexpr int SD = TB_SMALL_DEPTH;
   constexpr int HD = TB_HEAVY_DEPTH;
   constexpr bool HG = TB_HEAVY_GA != 0;
-  for (int it = gw; it < 2 * n; it += W) {
-    if (it < n) {  // forward item: level-1 block k = it
-      const int k = it;
-      wait_flags(P, P.fflag, P.fdep, P.fdep_ptr[k], P.fdep_ptr[k + 1], epoch);
-      if (P.small[k] & 1)
-        sweep_lean::lane_chain<true, KS, 32, true, SD>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d,
-                                                       src, mid, 32, P.b_s, k, lane, ys, offs,
-                                                       lens);
-      else
-        sweep_lean::lane_chain<true, KC, 32, true, HD, HG>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d, src,
-                                                   mid, 32, P.b_s, k, lane, ys, offs, lens);
-      __syncwarp();
-      if (lane == 0) st_release(P.fflag + k, epoch);
-    } else {  // backward item: level-1 block k = 2n-1-it (colors descending)
-      const int k = 2 * n - 1 - it;
-      // deps: own rows' rhs (= forward result of block k) + later-color blocks
-      wait_flags(P, P.bflag, P.bdep, P.bdep_ptr[k], P.bdep_ptr[k + 1], epoch, P.fflag + k);
-      if (P.small[k] & 2)
-        sweep_lean::lane_chain<false, KS, 32, true, SD>(P.Usp, P.Usl, P.Ucol, P.Uval,
-                                                        P.inv_d, mid, dst, 32, P.b_s, k, lane,
-                                                        ys, offs, lens, dotv, &dot);
-      else
-        sweep_lean::lane_chain<false, KC, 32, true, HD, HG>(P.Usp, P.Usl, P.Ucol, P.Uval, P.inv_d,
-                                                    mid, dst, 32, P.b_s, k, lane, ys, offs,
-                                                    lens, dotv, &dot);
-      __syncwarp();
-      if (lane == 0) st_release(P.bflag + k, epoch);
+  // Item sequence.  TB_PAIR_LAST (default): [forward items of colors
+  // 0..n_c-2] [(forward k, backward k) pairs of the last color, one warp
+  // doing both back to back] [backward items of colors n_c-2..0, k
+  // descending]: the last color's backward chains (their rhs is the forward
+  // result just written) run interleaved with the heavy forward ones instead
+  // of as a separate, latency-bound wave.  Otherwise forward k ascending then
+  // backward k descending.  Either way every dependency of an item has a
+  // lower sequence index.
+  const int L0 = TB_PAIR_LAST ? P.color_lvl1[P.n_c - 1] : n;
+  const int total = TB_PAIR_LAST ? n + L0 : 2 * n;
+  auto fwd_item = [&](int k) {
+    wait_flags(P, P.fflag, P.fdep, P.fdep_ptr[k], P.fdep_ptr[k + 1], epoch);
+    if (P.small[k] & 1)
+      sweep_lean::lane_chain<true, KS, 32, true, SD>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d,
+                                                     src, mid, 32, P.b_s, k, lane, ys, offs,
+                                                     lens);
+    else
+      sweep_lean::lane_chain<true, KC, 32, true, HD, HG>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d,
+                                                         src, mid, 32, P.b_s, k, lane, ys, offs,
+                                                         lens);
+    __syncwarp();
+    if (lane == 0) st_release(P.fflag + k, epoch);
+  };
+  auto bwd_item = [&](int k) {
+    // deps: own rows' rhs (= forward result of block k) + later-color blocks
+    wait_flags(P, P.bflag, P.bdep, P.bdep_ptr[k], P.bdep_ptr[k + 1], epoch, P.fflag + k);
+    if (P.small[k] & 2)
+      sweep_lean::lane_chain<false, KS, 32, true, SD>(P.Usp, P.Usl, P.Ucol, P.Uval, P.inv_d,
+                                                      mid, dst, 32, P.b_s, k, lane, ys, offs,
+                                                      lens, dotv, &dot);
+    else
+      sweep_lean::lane_chain<false, KC, 32, true, HD, HG>(P.Usp, P.Usl, P.Ucol, P.Uval,
+                                                          P.inv_d, mid, dst, 32, P.b_s, k, lane,
+                                                          ys, offs, lens, dotv, &dot);
+    __syncwarp();
+    if (lane == 0) st_release(P.bflag + k, epoch);
+  };
+  for (int it = gw; it < total; it += W) {
+    if (it < L0) {
+      fwd_item(it);
+    } else if (it < n) {
+      if (TB_PAIR_LAST) {
+        fwd_item(it);
+        bwd_item(it);
+      } else {
+        fwd_item(it);
+      }
+    } else {
+      bwd_item(TB_PAIR_LAST ? L0 - 1 - (it - n) : 2 * n - 1 - it);
     }
   }
   return dot;
