@@ -16,6 +16,8 @@
 // per color, thread per (level-1 block, lane) walking its b_s rows in order,
 // computes every row after all rows it reads: earlier colors finished in
 // earlier launches, earlier steps of the same lane by the same thread.
+// The kernel checks that precondition per entry (a violation fails the call
+// with TB_EINVAL instead of computing from unfinished rows).
 // A non-positive pivot records min(row) with atomicMin; a row's dependents
 // all have larger indices, so the minimum is the row the sequential
 // reference stops at, and its pivot is exact.
@@ -39,16 +41,26 @@ namespace {
 __global__ void __launch_bounds__(128)
     ic0_phase(const long long *__restrict__ lrp, const int *__restrict__ lci, double *lv,
               const double *__restrict__ adiag, double *d, double *inv_d, int w, int b_s,
-              long long k0, long long nthreads, unsigned long long *bad_row, double *pivots) {
+              long long k0, long long nthreads, unsigned long long *bad_row, double *pivots,
+              unsigned *bad_structure) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= nthreads) return;
   const long long k = k0 + g / w;
   const int j = (int)(g % w);
+  const long long span = (long long)b_s * w;
   for (int l = 0; l < b_s; ++l) {
     const long long i = (k * b_s + l) * w + j;
     const long long lo = lrp[i], hi = lrp[i + 1];
     for (long long p = lo; p < hi; ++p) {
       const int jc = lci[p];
+      // the schedule's precondition: same block => same lane, earlier step;
+      // else an earlier color (its level-1 blocks all precede k0)
+      const long long kj = jc / span;
+      const bool ok = kj == k ? ((jc % w) == j && jc < i) : kj < k0;
+      if (!ok) {
+        atomicOr(bad_structure, 1u);
+        return;
+      }
       double s = lv[p];
       long long p1 = lo, p2 = lrp[jc];
       const long long e2 = lrp[jc + 1];
@@ -94,22 +106,27 @@ extern "C" int tb_dev_ic0_hbmc(int64_t n, const int64_t *lrp, const int32_t *lci
     return fail(TB_EINVAL, "dev_ic0_hbmc: color ranges do not cover n");
   if (n > 0x7fffffffLL) return fail(TB_EINVAL, "dev_ic0_hbmc: n exceeds int32 columns");
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned long long *flag = nullptr;
-  CU(cudaMallocAsync((void **)&flag, sizeof(unsigned long long), s));
+  unsigned long long *flag = nullptr;   // [0] = min bad row, [1] = structure error
+  CU(cudaMallocAsync((void **)&flag, 2 * sizeof(unsigned long long), s));
   CU(cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), s));
+  CU(cudaMemsetAsync(flag + 1, 0, sizeof(unsigned long long), s));
   for (int64_t c = 0; c < n_c; ++c) {
     const long long k0 = color_lvl1_ranges[c], k1 = color_lvl1_ranges[c + 1];
     const long long nt = (k1 - k0) * w;
     if (nt <= 0) continue;
     ic0_phase<<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(
         (const long long *)lrp, lci, lvals, adiag, d, inv_d, (int)w, (int)b_s, k0, nt, flag,
-        pivot_ws);
+        pivot_ws, (unsigned *)(flag + 1));
     CU(cudaGetLastError());
   }
-  unsigned long long h = ~0ULL;
-  CU(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, s));
+  unsigned long long hf[2] = {~0ULL, 0};
+  CU(cudaMemcpyAsync(hf, flag, sizeof(hf), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   CU(cudaFreeAsync(flag, s));
+  if (hf[1])
+    return fail(TB_EINVAL, "dev_ic0_hbmc: matrix lacks the HBMC dependency structure "
+                "(a strictly-lower entry is neither same-lane-earlier-step nor an earlier color)");
+  const unsigned long long h = hf[0];
   if (h != ~0ULL) {
     *bad_row = (int64_t)h;
     CU(cudaMemcpy(bad_pivot, pivot_ws + h, sizeof(double), cudaMemcpyDeviceToHost));

@@ -3,7 +3,7 @@
 # under a host-memory watchdog (kill above 170 GB RSS).
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 free -g | head -2
-for n in 256 512; do
+for n in ${C5_SIZES:-256 512}; do
   python scripts/run_config5.py $n 5 > gpurun_out/config5_$n.log 2>&1 &
   pid=$!
   while kill -0 $pid 2>/dev/null; do

@@ -116,6 +116,25 @@ if os.environ.get("C5_ORACLE", "1") == "1":
     out["oracle_threads"] = O.max_threads()
     print("oracle parity", out["fwd_bitwise"], out["bwd_bitwise"], flush=True)
 
+# IC(0): host builder (what prepare() ran) vs the device factorization
+if os.environ.get("C5_IC0", "1") == "1":
+    from paper_1908_00741_b200 import precond as PC
+    t0 = time.perf_counter()
+    fh = PC.ic0_factorize(st.a_sys, layout_tag="hbmc")
+    out["ic0_host_s"] = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tk = {}
+    fd = PC.ic0_factorize_device(st.a_sys, hl, timings=tk)
+    out["ic0_device_s"] = time.perf_counter() - t0   # incl. checks, H2D of the pattern, D2H
+    out["ic0_device_kernels_s"] = tk["kernel_s"]
+    out["ic0_device_bitwise"] = bool(np.array_equal(fd.L.vals, fh.L.vals) and
+                                     np.array_equal(fd.d, fh.d) and
+                                     np.array_equal(fd.inv_diag, fh.inv_diag))
+    del fh, fd
+    print("ic0 host", out["ic0_host_s"], "device", out["ic0_device_s"],
+          out["ic0_device_bitwise"], flush=True)
+
 bd = torch.from_numpy(st.b_sys).cuda()
 xd = torch.empty_like(bd)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

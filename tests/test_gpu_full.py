@@ -301,3 +301,15 @@ def test_p2p_transport_pcg_full_config2(P):
     cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
     x, rep = distributed.pcg_partitioned(a, b, cfg, 2, transport="p2p")
     _check_against_digest(rep, x, dg)
+
+
+def test_device_ic0_rejects_non_hbmc_structure(P):
+    """A matrix not in HBMC order (natural order of a 2-D grid) must be
+    refused, not factored from rows the schedule has not finished."""
+    from paper_1908_00741_b200 import precond
+    a, _ = P.gen_laplacian_5pt(16, 16)
+    lay = P.color_blocks(a, P.build_blocks(a, 4))
+    hl = P.build_hbmc(lay, 8)
+    a_ext, _ = P.extend_with_dummies(a, np.zeros(a.n), hl)
+    with pytest.raises(ValueError, match="dependency structure"):
+        precond.ic0_factorize_device(a_ext, hl)     # not permuted into HBMC order
