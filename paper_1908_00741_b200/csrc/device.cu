@@ -430,6 +430,9 @@ __global__ void __launch_bounds__(kBlock)
   TB_GRID_STRIDE4({ p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i])); })
 }
 
+// Next preconditioner epoch for graph-replayed dataflow launches.
+__global__ void epoch_bump(unsigned *e) { *e += 1u; }
+
 // ------------------------------------------------------------ persistent
 // Whole preconditioner application (mode 0) or whole PCG solve (mode 1) in
 // one cooperative launch; see persist.cuh.  Writes the final PcgState.
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(persist::kThreads, TB_PMINB)
     return d;
   };
   if (P.mode == 0) {
-    precond(P.pre_src, P.pre_dst, P.epoch, nullptr);
+    precond(P.pre_src, P.pre_dst, P.epoch_dev ? *P.epoch_dev : P.epoch, nullptr);
     return;
   }
   const double tol = st->tol;
@@ -815,6 +818,9 @@ struct tb_plan {
   // tb_pcg as a host-polled kernel sequence with the TMA SpMV and one
   // persistent dataflow precond launch per iteration (large systems)
   bool split_pcg = false;
+  bool in_graph = false;       // capturing the split graph: precond epochs from epoch_dev
+  bool g_split = false;        // the instantiated graph is the split variant
+  unsigned *epoch_dev = nullptr;
 };
 
 namespace {
@@ -1229,11 +1235,21 @@ int launch_precond_step(tb_plan *pl, cudaStream_t s, long long *nl) {
   int rc;
   if (pl->split_pcg) {
     if ((rc = launch_persistent(pl, 0, pl->r, pl->z, nullptr, nullptr, s, 1))) return rc;
-    ++*nl;
+    *nl += pl->in_graph ? 2 : 1;   // + the epoch bump
     return TB_OK;
   }
   if ((rc = launch_forward(pl, pl->r, pl->y, s, pl->st, nl))) return rc;
   return launch_backward(pl, pl->y, pl->z, s, pl->st, nl);
+}
+
+// TB_DEBUG_SYNC=1 (diagnostics, never inside a graph capture): synchronise
+// after every stage of a kernel-sequence iteration and name the failing one.
+int debug_sync(tb_plan *pl, cudaStream_t s, const char *stage) {
+  if (pl->in_graph || !env_int("TB_DEBUG_SYNC", 0)) return TB_OK;
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess)
+    return fail(TB_ECUDA, "%s failed: %s", stage, cudaGetErrorString(e));
+  return TB_OK;
 }
 
 int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
@@ -1241,13 +1257,18 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   const unsigned rg = reduce_grid(n);
   int rc;
   if ((rc = launch_spmv(pl, pl->p, pl->ap, s, true, nl))) return rc;
+  if ((rc = debug_sync(pl, s, "spmv+dot"))) return rc;
   cg_update_xr<<<rg, kBlock, 0, s>>>(n, pl->p, pl->ap, x, pl->r, pl->partials,
                                      pl->st, pl->hist);
   ++*nl;
+  if ((rc = debug_sync(pl, s, "cg_update_xr"))) return rc;
   if ((rc = launch_precond_step(pl, s, nl))) return rc;
+  if ((rc = debug_sync(pl, s, "precond"))) return rc;
   cg_rz<false><<<rg, kBlock, 0, s>>>(n, pl->r, pl->z, pl->p, pl->partials, pl->st);
+  if ((rc = debug_sync(pl, s, "cg_rz"))) return rc;
   cg_update_p<<<reduce_grid(n), kBlock, 0, s>>>(n, pl->z, pl->p, pl->st);
   *nl += 2;
+  if ((rc = debug_sync(pl, s, "cg_update_p"))) return rc;
   CU(cudaGetLastError());
   return TB_OK;
 }
@@ -1290,11 +1311,14 @@ int build_graph(tb_plan *pl, const double *b, double *x) {
 
   // prologue captured into the root graph
   long long nl = 0;
+  pl->in_graph = pl->split_pcg;
+  pl->g_split = pl->split_pcg;
   CU(cudaStreamBeginCaptureToGraph(pl->stream, g, nullptr, nullptr, 0,
                                    cudaStreamCaptureModeThreadLocal));
   int rc = launch_prologue(pl, b, x, pl->stream, &nl);
   cudaGraph_t captured;
   cudaError_t ce = cudaStreamEndCapture(pl->stream, &captured);
+  if (rc || ce != cudaSuccess) pl->in_graph = false;
   if (rc) return rc;
   CU(ce);
   pl->launches_prologue = nl;
@@ -1324,6 +1348,7 @@ int build_graph(tb_plan *pl, const double *b, double *x) {
                                    cudaStreamCaptureModeThreadLocal));
   rc = launch_iteration(pl, x, pl->stream, &nl);
   ce = cudaStreamEndCapture(pl->stream, &captured);
+  pl->in_graph = false;
   if (rc) return rc;
   CU(ce);
   pl->launches_per_iter = nl;
@@ -1478,6 +1503,15 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
 
 // mode 0: z = M r (src -> dst); mode 1: whole PCG (b, x; state preset).
 // `applications` = preconditioner applications the launch may perform (epochs).
+void pcg_persistent_fn_launch(tb_plan *pl, const persist::Params &P, cudaStream_t s) {
+  switch (pl->persist_kc) {
+    case 2: pcg_persistent<2, true><<<pl->persist_grid, persist::kThreads, pl->persist_smem, s>>>(P); break;
+    case 4: pcg_persistent<4, true><<<pl->persist_grid, persist::kThreads, pl->persist_smem, s>>>(P); break;
+    case 6: pcg_persistent<6, true><<<pl->persist_grid, persist::kThreads, pl->persist_smem, s>>>(P); break;
+    default: pcg_persistent<8, true><<<pl->persist_grid, persist::kThreads, pl->persist_smem, s>>>(P); break;
+  }
+}
+
 int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, const double *b,
                       double *x, cudaStream_t s, long long applications) {
   persist::Params P;
@@ -1538,6 +1572,24 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.state = pl->st;
   P.watchdog = 4000000000LL;  // ~2 s at 1.9 GHz per barrier wait
   void *args[] = {&P};
+  if (mode == 0 && P.n_lvl1 > 0 && pl->in_graph) {
+    // captured into the split PCG graph: the epoch comes from device memory
+    // (bumped by a 1-thread kernel after each application) and the launch is
+    // a plain one -- the dataflow schedule has no grid barrier, and the
+    // graph runs its kernels one after another, so the grid is resident
+    P.epoch_dev = pl->epoch_dev;
+    if (env_int("TB_GRAPH_COOP", 0)) {
+      void *a2[] = {&P};
+      CU(cudaLaunchCooperativeKernel((const void *)persist_fn(pl->persist_kc, true),
+                                     dim3(pl->persist_grid), dim3(persist::kThreads), a2,
+                                     pl->persist_smem, s));
+    } else {
+      pcg_persistent_fn_launch(pl, P, s);
+    }
+    epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
+    CU(cudaGetLastError());
+    return TB_OK;
+  }
   if (mode == 0 && P.n_lvl1 > 0 && pl->pre_grid > 0) {
     CU(cudaLaunchCooperativeKernel((const void *)pre_fn(pl->persist_kc), dim3(pl->pre_grid),
                                    dim3(persist::kThreads), args, pl->persist_smem, s));
@@ -1752,6 +1804,7 @@ extern "C" int tb_plan_destroy(tb_plan *pl) {
   cudaFree(pl->color_lvl1_dev);
   cudaFree(pl->bar);
   cudaFree(pl->ppartials);
+  cudaFree(pl->epoch_dev);
   cudaFree(pl->fdep_ptr);
   cudaFree(pl->fdep);
   cudaFree(pl->bdep_ptr);
@@ -1884,6 +1937,21 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
     CU(cudaMalloc((void **)&pl->hist, sizeof(double) * (size_t)(max_iters + 1)));
     pl->hist_cap = max_iters + 1;
   }
+  // Split path (large systems): kernel sequence with the TMA SpMV and one
+  // persistent dataflow precond launch per iteration, host polling every
+  // check_every iterations (each launch takes a fresh flag epoch).
+  // TB_PCG_SPLIT=1/0 forces it on/off; default: n >= TB_PCG_SPLIT_N.
+  {
+    const int se = env_int("TB_PCG_SPLIT", -1);
+    const long long sn = (long long)env_int("TB_PCG_SPLIT_N", kSplitN);
+    // default only with the double-buffered TMA SpMV (short rows: configs
+    // 1, 2, 5); long rows (27-point) measured faster in the single launch
+    pl->split_pcg = pl->persist_ok && pl->n_lvl1_flow > 0 && pl->spmv_S > 0 &&
+                    (se == 1 || (se < 0 && pl->n >= sn && pl->spmv_D >= 2));
+    // the split path runs as a CUDA graph (conditional WHILE, device-side
+    // convergence test) unless TB_PCG_SPLIT_POLL=n asks for host polling
+    if (pl->split_pcg && check_every <= 0) check_every = env_int("TB_PCG_SPLIT_POLL", 0);
+  }
   // reset the device state (keep the loop handle if a graph exists)
   PcgState hs;
   CU(cudaMemcpy(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost));
@@ -1897,20 +1965,8 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
   CU(cudaMemcpy(pl->st, &hs, sizeof(PcgState), cudaMemcpyHostToDevice));
   int rc;
   long long polled_launches = 0, polls = 0;
-  // Split path (large systems): kernel sequence with the TMA SpMV and one
-  // persistent dataflow precond launch per iteration, host polling every
-  // check_every iterations (each launch takes a fresh flag epoch).
-  // TB_PCG_SPLIT=1/0 forces it on/off; default: n >= TB_PCG_SPLIT_N.
-  {
-    const int se = env_int("TB_PCG_SPLIT", -1);
-    const long long sn = (long long)env_int("TB_PCG_SPLIT_N", kSplitN);
-    // default only with the double-buffered TMA SpMV (short rows: configs
-    // 1, 2, 5); long rows (27-point) measured faster in the single launch
-    pl->split_pcg = pl->persist_ok && pl->n_lvl1_flow > 0 && pl->spmv_S > 0 &&
-                    (se == 1 || (se < 0 && pl->n >= sn && pl->spmv_D >= 2));
-    if (pl->split_pcg && check_every <= 0) check_every = env_int("TB_PCG_SPLIT_POLL", 4);
-  }
-  const bool persistent = check_every <= 0 && pl->persist_ok && pl->persist_pcg_ok;
+  const bool persistent =
+      check_every <= 0 && pl->persist_ok && pl->persist_pcg_ok && !pl->split_pcg;
   if (persistent) {
     if ((rc = sync_in(pl, stream))) return rc;
     if ((rc = launch_persistent(pl, 1, nullptr, nullptr, b, x, pl->stream, max_iters + 1)))
@@ -1934,13 +1990,30 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
     tmp.has_loop = has;
     CU(cudaMemcpy(pl->st, &tmp, sizeof(PcgState), cudaMemcpyHostToDevice));
   } else {
-    if (!pl->gexec || pl->g_b != b || pl->g_x != x || pl->g_hist_cap != pl->hist_cap) {
+    if (pl->split_pcg && !pl->epoch_dev) {
+      CU(cudaMalloc((void **)&pl->epoch_dev, sizeof(unsigned)));
+    }
+    if (!pl->gexec || pl->g_b != b || pl->g_x != x || pl->g_hist_cap != pl->hist_cap ||
+        pl->g_split != pl->split_pcg) {
       rc = build_graph(pl, b, x);
       if (rc) return rc;
     }
     if ((rc = sync_in(pl, stream))) return rc;
+    if (pl->split_pcg) {
+      // flags hold epochs < pl->epoch; restart them well before the
+      // counter could wrap during this solve
+      if ((unsigned long long)pl->epoch + (unsigned long long)max_iters + 4 > 0xF0000000ull) {
+        CU(cudaMemsetAsync(pl->flags, 0, sizeof(unsigned) * 2 * pl->n_lvl1_flow, pl->stream));
+        pl->epoch = 1;
+      }
+      CU(cudaMemcpyAsync(pl->epoch_dev, &pl->epoch, sizeof(unsigned), cudaMemcpyHostToDevice,
+                         pl->stream));
+    }
     CU(cudaGraphLaunch(pl->gexec, pl->stream));
     CU(cudaMemcpyAsync(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost, pl->stream));
+    if (pl->split_pcg)
+      CU(cudaMemcpyAsync(&pl->epoch, pl->epoch_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                         pl->stream));
     CU(cudaStreamSynchronize(pl->stream));
   }
   pl->split_pcg = false;

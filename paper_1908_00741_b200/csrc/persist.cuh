@@ -75,6 +75,7 @@ struct Params {
   unsigned long long *trace;   // optional phase timestamps (TB_TRACE), or null
   int n_lvl1;             // 0 = use the barrier-separated color phases
   unsigned epoch;         // epoch of the first preconditioner application
+  const unsigned *epoch_dev;  // mode 0 in a CUDA graph: epoch read from here (else null)
 };
 
 __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }

@@ -41,7 +41,7 @@ out["N"], out["nnz_A"] = int(a.n), int(a.nnz)
 print("generated", out, f"rss {rss_gb():.1f} GB", flush=True)
 cfg = P.CgConfig(ordering="hbmc", b_s=16, w=32, spmv_format="sell")
 t0 = time.perf_counter()
-st = solver.prepare(a, b, cfg)
+st = solver.prepare(a, b, cfg, ic0=os.environ.get("C5_PREP_IC0", "auto"))
 out["host_setup_s"] = time.perf_counter() - t0
 hl = st.layout
 out["n_c"], out["n_pad"], out["n_dummy"] = int(hl.n_c), int(hl.n_pad), int(hl.n_dummy)

@@ -313,3 +313,33 @@ def test_device_ic0_rejects_non_hbmc_structure(P):
     a_ext, _ = P.extend_with_dummies(a, np.zeros(a.n), hl)
     with pytest.raises(ValueError, match="dependency structure"):
         precond.ic0_factorize_device(a_ext, hl)     # not permuted into HBMC order
+
+
+def test_pcg_paths_interleaved_on_one_plan(P, monkeypatch):
+    """Graph-replayed split path, host-polled split path, single persistent
+    launch and the graph again, on one plan: same iterations, same x (the
+    dots are the same fixed-shape trees per path; paths may differ in the
+    last bits)."""
+    import torch
+    from paper_1908_00741_b200 import solver
+    g = load_golden("var7_16_b8_w32")
+    a, bs, w, _ = golden_matrix("var7_16_b8_w32")
+    from paper_1908_00741_b200 import problems
+    _, b = problems.rhs(a)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    st = solver.attach_plan(solver.prepare(a, b, cfg), cfg)
+    bd = torch.from_numpy(st.b_sys).cuda()
+    xd = torch.empty_like(bd)
+    out = []
+    for env in ({}, {"TB_PCG_SPLIT_POLL": "3"}, {"TB_PCG_SPLIT": "0"}, {}, {"TB_PCG_SPLIT_POLL": "1"}):
+        for k in ("TB_PCG_SPLIT_POLL", "TB_PCG_SPLIT"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        rep, hist = st.plan.pcg(bd, xd, cfg.tol, cfg.max_iters)
+        x = xd.cpu().numpy()[st.old_positions]
+        assert abs(rep.iterations - int(g["pcg_hbmc_iters"])) <= 1
+        assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
+        out.append(x)
+    assert np.array_equal(out[0], out[3])     # graph replay is deterministic
+    st.plan.close()
