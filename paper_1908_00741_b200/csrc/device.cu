@@ -818,6 +818,7 @@ struct tb_plan {
   // tb_pcg as a host-polled kernel sequence with the TMA SpMV and one
   // persistent dataflow precond launch per iteration (large systems)
   bool split_pcg = false;
+  int vec_pt = 16;             // elements per thread of the CG vector kernels (grid size)
   bool in_graph = false;       // capturing the split graph: precond epochs from epoch_dev
   bool g_split = false;        // the instantiated graph is the split variant
   unsigned *epoch_dev = nullptr;
@@ -1254,7 +1255,7 @@ int debug_sync(tb_plan *pl, cudaStream_t s, const char *stage) {
 
 int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   const long long n = pl->n;
-  const unsigned rg = reduce_grid(n);
+  const unsigned rg = reduce_grid(n, pl->vec_pt);
   int rc;
   if ((rc = launch_spmv(pl, pl->p, pl->ap, s, true, nl))) return rc;
   if ((rc = debug_sync(pl, s, "spmv+dot"))) return rc;
@@ -1266,7 +1267,7 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   if ((rc = debug_sync(pl, s, "precond"))) return rc;
   cg_rz<false><<<rg, kBlock, 0, s>>>(n, pl->r, pl->z, pl->p, pl->partials, pl->st);
   if ((rc = debug_sync(pl, s, "cg_rz"))) return rc;
-  cg_update_p<<<reduce_grid(n), kBlock, 0, s>>>(n, pl->z, pl->p, pl->st);
+  cg_update_p<<<reduce_grid(n, pl->vec_pt), kBlock, 0, s>>>(n, pl->z, pl->p, pl->st);
   *nl += 2;
   if ((rc = debug_sync(pl, s, "cg_update_p"))) return rc;
   CU(cudaGetLastError());
@@ -1705,6 +1706,8 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
   pl->spmv_format = d->spmv_format;
   pl->n = d->n;
   pl->n_real = d->n_real;
+  pl->vec_pt = env_int("TB_VEC_PT", 16);   // A/B: 16 > 8 > 4 > 32 (profiles/README.md)
+  if (pl->vec_pt < 1) pl->vec_pt = 1;
   int rc = TB_OK;
   auto bail = [&](int code) {
     tb_plan_destroy(pl);

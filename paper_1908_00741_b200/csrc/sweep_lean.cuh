@@ -29,6 +29,9 @@
 #ifndef TB_LEAN_MINB
 #define TB_LEAN_MINB 1
 #endif
+#ifndef TB_PF_L2
+#define TB_PF_L2 0
+#endif
 
 namespace sweep_lean {
 
@@ -129,11 +132,31 @@ __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_p
 
   if constexpr (DEPTH <= 2 && !GA) {
     Buf<KC> A, B;
+    // TB_PF_L2 = d > 0: at step i, also prefetch into L2 the operand lines of
+    // step i + d (prefetch.global.L2: fire-and-forget, no destination
+    // register), so the register ping-pong's loads hit L2 instead of DRAM.
+    auto prefetch = [&](int i) {
+      if (TB_PF_L2 <= 0 || i >= b_s) return;
+      const int off = offs[i * nt + tid], len = lens[i * nt + tid];
+      const int row = blk0 + (FWD ? i : b_s - 1 - i) * w + j;
+#pragma unroll
+      for (int u = 0; u < KC; ++u)
+        if (u < len) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(val + off + u * w));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(col + off + u * w));
+        }
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src + row));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(inv_d + row));
+    };
+    if (TB_PF_L2 > 0)
+      for (int q = 1; q <= TB_PF_L2 && q < b_s; ++q) prefetch(q);
     load(0, A);
     int i = 0;
     for (; i + 1 < b_s; i += 2) {
+      prefetch(i + 1 + TB_PF_L2);
       load(i + 1, B);
       step(i, A);
+      prefetch(i + 2 + TB_PF_L2);
       if (i + 2 < b_s) load(i + 2, A);
       step(i + 1, B);
     }
