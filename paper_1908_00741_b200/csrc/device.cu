@@ -1468,6 +1468,14 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
     };
     build(d->L_sell, fp, fd, true);
     build(d->U_sell, bp, bd, false);
+    // Long dependency lists (the kNN graph with algebraic numbering: ~300
+    // source blocks per level-1 block) make the per-item flag polls cost
+    // more than the barriers they replace (ICCG 223 vs 166 ms at config 4);
+    // structured configs have 2.5 (config 2) / 9.9 (config 3) on average.
+    if (ok && nl > 0) {
+      const double avg = (double)(fd.size() > bd.size() ? fd.size() : bd.size()) / (double)nl;
+      if (avg > (double)env_int("TB_FLOW_MAXDEP", 64)) ok = false;
+    }
     if (ok && nl > 0) {
       if (fd.empty()) fd.push_back(0);
       if (bd.empty()) bd.push_back(0);
