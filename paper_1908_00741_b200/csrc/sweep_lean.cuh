@@ -32,9 +32,6 @@
 #ifndef TB_PF_L2
 #define TB_PF_L2 0
 #endif
-#ifndef TB_LONG_CHUNK
-#define TB_LONG_CHUNK 0
-#endif
 
 namespace sweep_lean {
 
@@ -118,35 +115,13 @@ __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_p
 #pragma unroll
     for (int u = 0; u < KC; ++u)
       if (u < len) update(b.c[u], b.v[u], x[u]);
-    if (len > KC) {  // long row: the remaining slots
+    if (len > KC) {  // long row: remaining slots synchronously
       const int off = offs[i * nt + tid];
-      if (TB_LONG_CHUNK > 1) {
-        // TB_LONG_CHUNK slots' loads and gathers in flight together
-        constexpr int LC = TB_LONG_CHUNK > 1 ? TB_LONG_CHUNK : 2;
-        for (int t0 = KC; t0 < len; t0 += LC) {
-          int cc[LC];
-          double vv[LC], xc[LC];
-#pragma unroll
-          for (int u = 0; u < LC; ++u) {
-            const bool in = t0 + u < len;
-            cc[u] = in ? __ldg(col + off + (t0 + u) * w) : row;
-            vv[u] = in ? __ldg(val + off + (t0 + u) * w) : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < LC; ++u)
-            xc[u] = (t0 + u < len && (unsigned)(cc[u] - blk0) >= uspan) ? ldv<CG>(dst + cc[u])
-                                                                       : 0.0;
-#pragma unroll
-          for (int u = 0; u < LC; ++u)
-            if (t0 + u < len) update(cc[u], vv[u], xc[u]);
-        }
-      } else {
-        for (int t = KC; t < len; ++t) {
-          const int cc = __ldg(col + off + t * w);
-          const double vv = __ldg(val + off + t * w);
-          const double xc = (unsigned)(cc - blk0) < uspan ? 0.0 : ldv<CG>(dst + cc);
-          update(cc, vv, xc);
-        }
+      for (int t = KC; t < len; ++t) {
+        const int cc = __ldg(col + off + t * w);
+        const double vv = __ldg(val + off + t * w);
+        const double xc = (unsigned)(cc - blk0) < uspan ? 0.0 : ldv<CG>(dst + cc);
+        update(cc, vv, xc);
       }
     }
     y = __dmul_rn(y, b.idg);
