@@ -397,6 +397,106 @@ __global__ void __launch_bounds__(kBlock)
   });
 }
 
+// ---- SpMV + p.Ap + alpha + x/r update + ||r|| in ONE cooperative launch
+// (split PCG path).  The TMA SpMV writes ap for this CTA's chunks; a
+// deterministic grid sum (every CTA adds the CTA partials in index order
+// after a grid barrier) gives p.Ap; alpha = rz / p.Ap; the same CTA then
+// updates x and r over the rows it just produced (p and ap are L2-hot) and a
+// second grid sum gives ||r||.  Saves the separate x/r pass's launch and its
+// DRAM re-reads of p and ap.  Semantics of spmv_tma_dot + cg_update_xr.
+__device__ __forceinline__ void coop_sync(unsigned *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned *gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      const long long t0 = clock64();
+      while (*gen == g)
+        if (clock64() - t0 > 4000000000LL) __trap();
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double coop_sum(double v, double *partials, unsigned *bar,
+                                           double *sh) {
+  const double bsum = block_sum(v, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = bsum;
+  coop_sync(bar);
+  double acc = 0.0;
+  if (threadIdx.x < 32) {
+    for (unsigned q = threadIdx.x; q < gridDim.x; q += 32) acc += __ldcg(partials + q);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) sh[32] = acc;
+  }
+  __syncthreads();
+  const double tot = sh[32];
+  __syncthreads();
+  return tot;
+}
+
+__global__ void __launch_bounds__(spmv_tma::kThreads, 2)
+    spmv_tma_xr(const __grid_constant__ spmv_tma::Params p, double *x, double *r,
+                double *partials, unsigned *bar, PcgState *st, double *hist) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double sh[33];
+  if (st->done) return;   // uniform: every CTA sees the same state
+  spmv_tma::init_bars(p, smem);
+  unsigned phase = 0;
+  const double part = spmv_tma::run<true>(p, smem, phase);
+  const double pap = coop_sum(part, partials, bar, sh);
+  const long long j = st->iter + 1;
+  const double rz = st->rz, bnorm = st->bnorm;
+  if (pap <= 0.0) {  // src/solver.py:176-177
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->pap = pap;
+      st->status = TB_ECG_BREAKDOWN;
+      st->bd_iter = j;
+      st->bd_val = pap;
+      stop_loop(st);
+    }
+    return;
+  }
+  const double alpha = rz / pap;
+  // x/r over the rows of this CTA's chunks (the rows run<> produced)
+  double rr = 0.0;
+  const long long rows_per_chunk = (long long)p.S * 32;
+  const long long n = p.n_slices * 32;
+  for (long long q = blockIdx.x; q < p.n_chunks; q += gridDim.x) {
+    const long long r0 = q * rows_per_chunk;
+    const long long r1 = r0 + rows_per_chunk < n ? r0 + rows_per_chunk : n;
+    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      const double pi = __ldcg(p.x + i), ai = __ldcg(p.out + i);
+      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
+      const double ri = __dsub_rn(r[i], __dmul_rn(alpha, ai));
+      r[i] = ri;
+      rr += ri * ri;
+    }
+  }
+  const double rrt = coop_sum(rr, partials + gridDim.x, bar, sh);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->pap = pap;
+    st->alpha = alpha;
+    const double rel = sqrt(rrt) / bnorm;
+    st->rel = rel;
+    st->iter = j;
+    hist[j] = rel;
+    if (rel < st->tol) {
+      st->converged = 1;
+      stop_loop(st);
+    } else if (j >= st->max_iters) {
+      stop_loop(st);
+    }
+  }
+}
+
 // rz_new = r . z; beta = rz_new / rz; rz = rz_new (src/solver.py:190-192).
 // FIRST: the prologue's rz = r . z and p = z.
 template <bool FIRST>
@@ -819,6 +919,7 @@ struct tb_plan {
   // persistent dataflow precond launch per iteration (large systems)
   bool split_pcg = false;
   int vec_pt = 16;             // elements per thread of the CG vector kernels (grid size)
+  int xr_grid = 0;             // spmv_tma_xr cooperative grid (0 = separate x/r pass)
   bool in_graph = false;       // capturing the split graph: precond epochs from epoch_dev
   bool g_split = false;        // the instantiated graph is the split variant
   unsigned *epoch_dev = nullptr;
@@ -1176,6 +1277,20 @@ int launch_backward(tb_plan *pl, const double *src, double *dst, cudaStream_t s,
   return TB_OK;
 }
 
+void spmv_params(const tb_plan *pl, const double *x, double *out, spmv_tma::Params &P) {
+  P.n_slices = pl->A.n_slices;
+  P.slice_ptr = pl->A.slice_ptr;
+  P.slice_len = pl->A.slice_len;
+  P.col = pl->A.col;
+  P.val = pl->A.val;
+  P.x = x;
+  P.out = out;
+  P.S = pl->spmv_S;
+  P.cap = pl->spmv_cap;
+  P.D = pl->spmv_D;
+  P.n_chunks = (pl->A.n_slices + P.S - 1) / P.S;
+}
+
 int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
                 bool dot, long long *nl) {
   const long long n = pl->n;
@@ -1184,17 +1299,7 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
     return fail(TB_EINVAL, "plan has no matrix A (preconditioner-only plan)");
   if (pl->spmv_format == TB_SPMV_SELL && pl->spmv_S > 0) {
     spmv_tma::Params P;
-    P.n_slices = pl->A.n_slices;
-    P.slice_ptr = pl->A.slice_ptr;
-    P.slice_len = pl->A.slice_len;
-    P.col = pl->A.col;
-    P.val = pl->A.val;
-    P.x = x;
-    P.out = out;
-    P.S = pl->spmv_S;
-    P.cap = pl->spmv_cap;
-    P.D = pl->spmv_D;
-    P.n_chunks = (pl->A.n_slices + P.S - 1) / P.S;
+    spmv_params(pl, x, out, P);
     if (dot)
       spmv_tma_dot<<<pl->spmv_grid, spmv_tma::kThreads, spmv_tma::smem_bytes(P.cap, P.D), s>>>(
           P, pl->partials, pl->st);
@@ -1257,12 +1362,27 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   const long long n = pl->n;
   const unsigned rg = reduce_grid(n, pl->vec_pt);
   int rc;
-  if ((rc = launch_spmv(pl, pl->p, pl->ap, s, true, nl))) return rc;
-  if ((rc = debug_sync(pl, s, "spmv+dot"))) return rc;
-  cg_update_xr<<<rg, kBlock, 0, s>>>(n, pl->p, pl->ap, x, pl->r, pl->partials,
-                                     pl->st, pl->hist);
-  ++*nl;
-  if ((rc = debug_sync(pl, s, "cg_update_xr"))) return rc;
+  if (pl->split_pcg && pl->xr_grid > 0) {
+    spmv_tma::Params P;
+    spmv_params(pl, pl->p, pl->ap, P);
+    double *xx = x, *rr = pl->r, *pp = pl->partials;
+    unsigned *bb = pl->bar;
+    PcgState *ss = pl->st;
+    double *hh = pl->hist;
+    void *args[] = {&P, &xx, &rr, &pp, &bb, &ss, &hh};
+    CU(cudaLaunchCooperativeKernel((const void *)spmv_tma_xr, dim3(pl->xr_grid),
+                                   dim3(spmv_tma::kThreads), args,
+                                   spmv_tma::smem_bytes(P.cap, P.D), s));
+    ++*nl;
+    if ((rc = debug_sync(pl, s, "spmv+xr"))) return rc;
+  } else {
+    if ((rc = launch_spmv(pl, pl->p, pl->ap, s, true, nl))) return rc;
+    if ((rc = debug_sync(pl, s, "spmv+dot"))) return rc;
+    cg_update_xr<<<rg, kBlock, 0, s>>>(n, pl->p, pl->ap, x, pl->r, pl->partials,
+                                       pl->st, pl->hist);
+    ++*nl;
+    if ((rc = debug_sync(pl, s, "cg_update_xr"))) return rc;
+  }
   if ((rc = launch_precond_step(pl, s, nl))) return rc;
   if ((rc = debug_sync(pl, s, "precond"))) return rc;
   cg_rz<false><<<rg, kBlock, 0, s>>>(n, pl->r, pl->z, pl->p, pl->partials, pl->st);
@@ -1679,6 +1799,17 @@ int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
     pl->spmv_cap = (int)cap;
     pl->spmv_D = c.D;
     pl->spmv_grid = per_sm * nsm;
+    // fused SpMV + x/r (cooperative): its own co-resident grid
+    if (env_int("TB_XR_FUSE", 0)) {   // off: 26.1 vs 24.5 ms at config 2 (profiles/README.md)
+      cudaFuncAttributes fa;
+      CU(cudaFuncGetAttributes(&fa, spmv_tma_xr));
+      CU(cudaFuncSetAttribute(spmv_tma_xr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - (int)fa.sharedSizeBytes));
+      int ps = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmv_tma_xr, spmv_tma::kThreads, sm));
+      if (ps > per_sm) ps = per_sm;
+      pl->xr_grid = ps > 0 ? ps * nsm : 0;
+    }
     return TB_OK;
   }
   return TB_OK;
