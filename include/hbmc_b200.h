@@ -350,6 +350,27 @@ int tb_p2p_push(int64_t n, const int32_t *idx, const double *src, double *dst_re
 int tb_p2p_wait(const uint32_t *flags, int32_t count, int32_t skip, uint32_t epoch,
                 void *stream);
 
+/* One color phase of a partitioned rank's sweep with the halo push FUSED
+ * into the sweep kernel: after a thread's lane walk, every row another rank
+ * needs is stored straight into that rank's vector (peer-mapped pointer),
+ * and the CTA finishing last releases `epoch` into each peer's flag word for
+ * this rank (system scope) -- no separate pack / send.  Requires the lean
+ * per-phase kernel (w = 32). */
+#define TB_MAX_PEERS 16
+typedef struct {
+    int64_t row0, nrows;        /* local rows of the phase: [row0, row0 + nrows) */
+    const int32_t *ptr;         /* device [nrows + 1]: destinations of row0 + r */
+    const int32_t *peer;        /* device: index into peer_dst / peer_flag */
+    const int32_t *off;         /* device: element index in that peer's vector */
+    int32_t npeers;
+    double *peer_dst[TB_MAX_PEERS];
+    uint32_t *peer_flag[TB_MAX_PEERS];
+    uint32_t epoch;
+    uint32_t *done_ctr;         /* device word, 0, private to this launch */
+} tb_push_desc;
+int tb_plan_sweep_phase_push(tb_plan *plan, int forward, int64_t phase, const double *src,
+                             double *dst, const tb_push_desc *push, void *stream);
+
 /* K/numba_backend.py:40-79 ic0_factor on the device, bitwise, for a system
  * in HBMC order (src/precond.py:179-200 with layout "hbmc"): one launch per
  * color, thread per (level-1 block, lane) walking its b_s rows.  lrp / lci /

@@ -62,6 +62,15 @@ class TbPlanDesc(C.Structure):
                 ("A_sell", TbSellHost), ("A_csr", TbCsrHost), ("flags", i64)]
 
 
+TB_MAX_PEERS = 16
+
+
+class TbPushDesc(C.Structure):
+    _fields_ = [("row0", i64), ("nrows", i64), ("ptr", vp), ("peer", vp), ("off", vp),
+                ("npeers", i32), ("peer_dst", vp * TB_MAX_PEERS),
+                ("peer_flag", vp * TB_MAX_PEERS), ("epoch", C.c_uint32), ("done_ctr", vp)]
+
+
 class TbPcgReport(C.Structure):
     _fields_ = [("iterations", i64), ("converged", i32), ("status", i32),
                 ("breakdown_iter", i64), ("breakdown_value", dbl),
@@ -109,6 +118,7 @@ _SIGS = {
     "tb_dev_dot": [i64, vp, vp, vp, i32, vp, vp],
     "tb_dev_cg_xr": [i64, vp, i32, i32, vp, vp, vp, vp, i32, vp, vp],
     "tb_dev_cg_p": [i64, vp, i32, i32, vp, vp, vp],
+    "tb_plan_sweep_phase_push": [vp, C.c_int, i64, vp, vp, C.POINTER(TbPushDesc), vp],
     "tb_p2p_alloc": [i64, C.POINTER(vp), vp],
     "tb_p2p_free": [vp],
     "tb_p2p_open": [vp, C.POINTER(vp)],

@@ -2022,6 +2022,52 @@ extern "C" int tb_plan_sweep_phase(tb_plan *pl, int forward, int64_t phase,
   return TB_OK;
 }
 
+extern "C" int tb_plan_sweep_phase_push(tb_plan *pl, int forward, int64_t phase,
+                                        const double *src, double *dst,
+                                        const tb_push_desc *push, void *stream) {
+  if (!pl || !push) return fail(TB_EINVAL, "sweep_phase_push: null argument");
+  if (pl->precond_kind != TB_PRECOND_HBMC || phase < 0 || phase >= pl->n_c)
+    return fail(TB_EINVAL, "sweep_phase_push: HBMC plan and 0 <= phase < n_c required");
+  if (pl->w != 32 || push->npeers < 0 || push->npeers > TB_MAX_PEERS || !push->done_ctr)
+    return fail(TB_EINVAL, "sweep_phase_push: w = 32 and 0 <= npeers <= %d required",
+                TB_MAX_PEERS);
+  const tb_plan::ColorLaunch &L = forward ? pl->cl_fwd[phase] : pl->cl_bwd[phase];
+  if (L.kind != 4 && L.k1 > L.k0)
+    return fail(TB_EINVAL, "sweep_phase_push: needs the lean phase kernel");
+  CU(cudaSetDevice(pl->device));
+  const cudaStream_t s = (cudaStream_t)stream;
+  const DevSell &M = forward ? pl->L : pl->U;
+  const long long nt = (L.k1 - L.k0) * 32;
+  const unsigned grid = nt > 0 ? grid_for(nt) : 1;
+  const size_t sm = sweep_lean::smem_bytes((int)pl->b_s, kBlock);
+  static bool attr = false;
+  if (!attr) {
+    int optin = 0;
+    CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
+    for (auto fn : {sweep_lean::sweep_push_kernel<true, 2>, sweep_lean::sweep_push_kernel<true, 4>,
+                    sweep_lean::sweep_push_kernel<true, 6>, sweep_lean::sweep_push_kernel<true, 8>,
+                    sweep_lean::sweep_push_kernel<false, 2>, sweep_lean::sweep_push_kernel<false, 4>,
+                    sweep_lean::sweep_push_kernel<false, 6>, sweep_lean::sweep_push_kernel<false, 8>}) {
+      cudaFuncAttributes fa;
+      CU(cudaFuncGetAttributes(&fa, fn));
+      CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - (int)fa.sharedSizeBytes));
+    }
+    attr = true;
+  }
+  auto pick = [&](auto f2, auto f4, auto f6, auto f8) {
+    return L.max_slots == 2 ? f2 : L.max_slots == 4 ? f4 : L.max_slots == 6 ? f6 : f8;
+  };
+  auto fn = forward ? pick(sweep_lean::sweep_push_kernel<true, 2>, sweep_lean::sweep_push_kernel<true, 4>,
+                           sweep_lean::sweep_push_kernel<true, 6>, sweep_lean::sweep_push_kernel<true, 8>)
+                    : pick(sweep_lean::sweep_push_kernel<false, 2>, sweep_lean::sweep_push_kernel<false, 4>,
+                           sweep_lean::sweep_push_kernel<false, 6>, sweep_lean::sweep_push_kernel<false, 8>);
+  fn<<<grid, kBlock, sm, s>>>(M.slice_ptr, M.slice_len, M.col, M.val, pl->inv_d, src, dst,
+                              (int)pl->b_s, (int)L.k0, (int)nt, *push);
+  CU(cudaGetLastError());
+  return TB_OK;
+}
+
 extern "C" int tb_plan_trace(const tb_plan *pl, uint64_t *out64) {
   if (!pl) return fail(TB_EINVAL, "null plan");
   if (!pl->trace) return fail(TB_EINVAL, "plan created without TB_TRACE=1");

@@ -253,6 +253,50 @@ __global__ void __launch_bounds__(256, TB_LEAN_MINB)
                                 k0 + kq, g - kq * w, ys, offs, lens);
 }
 
+// Per-phase lean sweep with the partitioned solve's halo push fused in
+// (tb_plan_sweep_phase_push, w = 32): after its walk a thread stores each of
+// its b_s results that peers need straight into their vectors (remote
+// stores over NVLink), then the last CTA out releases the phase's epoch into
+// every peer's flag for this rank.
+template <bool FWD, int KC>
+__global__ void __launch_bounds__(256, TB_LEAN_MINB)
+    sweep_push_kernel(const long long *__restrict__ slice_ptr, const int *__restrict__ slice_len,
+                      const int *__restrict__ col, const double *__restrict__ val,
+                      const double *__restrict__ inv_d, const double *__restrict__ src,
+                      double *__restrict__ dst, int b_s, int k0, int nthreads,
+                      const tb_push_desc pd) {
+  extern __shared__ __align__(16) double ys[];
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  int *offs = (int *)(ys + (size_t)b_s * blockDim.x);
+  int *lens = offs + (size_t)b_s * blockDim.x;
+  if (g < nthreads) {
+    const int kq = g >> 5, j = g & 31;
+    lane_chain<FWD, KC, 32, false>(slice_ptr, slice_len, col, val, inv_d, src, dst, 32, b_s,
+                                   k0 + kq, j, ys, offs, lens);
+    const long long blk0 = (long long)(k0 + kq) * b_s * 32;
+    for (int i = 0; i < b_s; ++i) {
+      const int l = FWD ? i : b_s - 1 - i;
+      const long long rel = blk0 + l * 32 + j - pd.row0;
+      if (rel < 0 || rel >= pd.nrows) continue;
+      const double y = ys[i * blockDim.x + threadIdx.x];
+      for (int q = pd.ptr[rel]; q < pd.ptr[rel + 1]; ++q) pd.peer_dst[pd.peer[q]][pd.off[q]] = y;
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(pd.done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    if (threadIdx.x == 0) *pd.done_ctr = 0;
+    __threadfence_system();
+    if (threadIdx.x < pd.npeers)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pd.peer_flag[threadIdx.x]),
+                   "r"(pd.epoch)
+                   : "memory");
+  }
+}
+
 __host__ inline size_t smem_bytes(int b_s, int threads) { return (size_t)b_s * threads * 16; }
 
 }  // namespace sweep_lean

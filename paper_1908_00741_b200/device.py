@@ -284,6 +284,12 @@ class DevicePlan:
                                       ptr(src), ptr(dst),
                                       stream if stream is not None else current_stream()))
 
+    def sweep_phase_push(self, forward, phase, src, dst, desc, stream=None):
+        """One color phase with the halo push fused in (tb_plan_sweep_phase_push)."""
+        check(LIB.tb_plan_sweep_phase_push(self.handle, 1 if forward else 0, int(phase),
+                                           ptr(src), ptr(dst), C.byref(desc),
+                                           stream if stream is not None else current_stream()))
+
     def phase_info(self, forward, phase):
         vals = [_lib.i32() for _ in range(4)]
         check(LIB.tb_plan_phase_info(self.handle, 1 if forward else 0, int(phase), *vals))

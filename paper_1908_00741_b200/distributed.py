@@ -57,6 +57,7 @@ class CudaRankOps:
         self.ws = t.empty(4096, dtype=t.float64, device="cuda")
         self.idx = {}
         self.plan = None
+        self.plan_lean = True
         if part.n_loc == 0:   # a rank with no level-1 block (tiny systems)
             return
         self.plan = D.DevicePlan(kind=_lib.TB_PRECOND_HBMC, n=part.n_loc, n_real=part.n_loc,
@@ -65,6 +66,10 @@ class CudaRankOps:
                                  L_sell=part.L, U_sell=part.U,
                                  spmv_format=_lib.TB_SPMV_SELL, A_sell=part.A,
                                  device=device, partitioned=True)
+        self.plan_lean = all(
+            self.plan.phase_info(f, c)["staged"] == 4 or
+            part.color_lvl1_ranges[c + 1] == part.color_lvl1_ranges[c]
+            for f in (True, False) for c in range(part.n_c))
 
     def stream(self):
         from . import device as D
@@ -167,7 +172,7 @@ class P2PTransport:
 
     NAMES = ("y", "z", "p")
 
-    def __init__(self, drv):
+    def __init__(self, drv, fused=True):
         import ctypes as C
         t = drv.ops[0].t
         self.t, self.drv = t, drv
@@ -212,6 +217,58 @@ class P2PTransport:
                         self.peer[rank][name] = ptr.value
                         self.opened.append(ptr.value)
         self.idx = {}
+        # fused sweep + push (tb_plan_sweep_phase_push): destinations per row
+        self.fused = fused
+        self.descs = {}
+
+    def _desc(self, i, kind, c, name, ex):
+        key = (i, kind, c, name)
+        d = self.descs.get(key)
+        if d is None:
+            p = self.drv.parts[i]
+            peers = [r for r in range(self.world) if r != p.rank]
+            slot = {r: q for q, r in enumerate(peers)}
+            dptr = self.t.from_numpy(ex.push_ptr).cuda()
+            dpeer = self.t.from_numpy(
+                np.array([slot[int(r)] for r in ex.push_rank], dtype=np.int32)).cuda()
+            doff = self.t.from_numpy(ex.push_off).cuda()
+            d = _lib.TbPushDesc()
+            d.row0 = ex.push_row0
+            d.nrows = ex.push_ptr.shape[0] - 1
+            d.ptr, d.peer, d.off = dptr.data_ptr(), dpeer.data_ptr(), doff.data_ptr()
+            d.npeers = len(peers)
+            for q, r in enumerate(peers):
+                d.peer_dst[q] = self.peer[r][name]
+                d.peer_flag[q] = self.peer[r]["flags"] + 4 * p.rank
+            d.done_ctr = self.bufs[i]["ctr"][0]
+            self.descs[key] = d = (d, (dptr, dpeer, doff))
+        return d[0]
+
+    def fused_phase(self, forward, c, src, dst, name):
+        """Color phase c of a sweep on every local rank with the halo push
+        fused into the sweep kernel, then each rank's stream waits for its
+        peers' flags (the exchange step of this phase)."""
+        from . import device as D
+        self.epoch = (self.epoch + 1) & 0x7fffffff
+        st = D.current_stream()
+        kind = "fwd" if forward else "bwd"
+        for i, p in enumerate(self.drv.parts):
+            ex = self.drv._ex(p, kind, c)
+            ops = self.drv.ops[i]
+            if ops.plan is not None:
+                desc = self._desc(i, kind, c, name, ex)
+                desc.epoch = self.epoch
+                ops.plan.sweep_phase_push(forward, c, src[i], dst[i], desc)
+            else:   # a rank without rows still releases its flags
+                for r in range(self.world):
+                    if r != p.rank:
+                        _lib.check(_lib.LIB.tb_p2p_push(0, None, None, None,
+                                                        self.peer[r]["flags"] + 4 * p.rank,
+                                                        self.epoch, self.bufs[i]["ctr"][0], st))
+            self.drv.bytes_sent += 8 * int(ex.push_off.shape[0]) if ex.push_off is not None else 0
+        for i, p in enumerate(self.drv.parts):
+            _lib.check(_lib.LIB.tb_p2p_wait(self.bufs[i]["flags"][0], self.world, p.rank,
+                                            self.epoch, st))
 
     def vec(self, i, name):
         return self.bufs[i][name][1][: self.drv.parts[i].n_ext]
@@ -261,7 +318,7 @@ class DistHbmc:
     per process under torch.distributed, with part.rank == dist rank).
     """
 
-    def __init__(self, parts, ops, group=None, transport="nccl"):
+    def __init__(self, parts, ops, group=None, transport="nccl", fused=True):
         self.parts = list(parts)
         self.ops = list(ops)
         self.world = self.parts[0].world
@@ -284,7 +341,7 @@ class DistHbmc:
                         self.sendbuf[(key_kind, c, i)] = self.ops[i].vec(ex.n_send)
         self.exchanges = 0
         self.bytes_sent = 0
-        self.p2p = P2PTransport(self) if transport == "p2p" else None
+        self.p2p = P2PTransport(self, fused=fused) if transport == "p2p" else None
 
     @staticmethod
     def _ex(p, kind, c):
@@ -370,7 +427,14 @@ class DistHbmc:
         """One substitution sweep on all local ranks with the per-color halo
         exchange (src/precond.py:377-392)."""
         order = range(self.n_c) if forward else range(self.n_c - 1, -1, -1)
+        last = self.n_c - 1 if forward else 0
+        fused = (self.p2p is not None and self.p2p.fused and self.parts[0].w == 32 and
+                 all(o.plan is None or o.plan_lean for o in self.ops))
         for c in order:
+            if fused and c != last:
+                self.p2p.fused_phase(forward, c, src, dst, self._p2p_name(dst))
+                self.exchanges += 1
+                continue
             for i in range(len(self.parts)):
                 self.ops[i].sweep_phase(forward, c, src[i], dst[i])
             self.exchange("fwd" if forward else "bwd", c, dst)

@@ -60,6 +60,13 @@ class Exchange:
     sends: list                   # [Msg] offsets into the send buffer
     recvs: list                   # [Msg] offsets into the extended vector
 
+    # fused push (sweep exchanges): per local row of the phase's color,
+    # its destinations (peer rank, element index in the peer's vector)
+    push_row0: int = 0
+    push_ptr: np.ndarray = None
+    push_rank: np.ndarray = None
+    push_off: np.ndarray = None
+
     @property
     def n_send(self):
         return int(self.send_idx.shape[0])
@@ -209,6 +216,7 @@ def partition_hbmc(L, U, A, inv_d, color_lvl1_ranges, b_s, w, world, ranks=None)
         for c in range(n_c):
             a, b = chunk_bounds(int(cr[c]), int(cr[c + 1]), world)[g]
             lcr[c + 1] = lcr[c] + (b - a)
+        lcr_ = lcr
         part = RankPart(rank=g, world=world, b_s=b_s, w=w, n_c=n_c, n_loc=n_loc,
                         n_halo=int(h.shape[0]), color_lvl1_ranges=lcr, lvl1=ks, rows=rows,
                         halo_rows=h, L=_local_sell(L, sids, w, n_loc, gmap),
@@ -252,7 +260,26 @@ def partition_hbmc(L, U, A, inv_d, color_lvl1_ranges, b_s, w, world, ranks=None)
                 if b > a:
                     recvs.append(Msg(s, n_loc + a, b - a))
             idx = (np.concatenate(send_idx) if send_idx else np.zeros(0, np.int64))
-            return Exchange(idx.astype(np.int32), sends, recvs)
+            ex = Exchange(idx.astype(np.int32), sends, recvs)
+            if kind != "spmv":
+                # rows of color c on this rank: [row0, row0 + nrows)
+                row0 = int(lcr_[c]) * span
+                nrows = int(lcr_[c + 1] - lcr_[c]) * span
+                rows_l = idx.astype(np.int64) - row0
+                rk = np.concatenate([np.full(m.count, m.peer, np.int64) for m in sends]) \
+                    if sends else np.zeros(0, np.int64)
+                ro = np.concatenate([m.remote_offset + np.arange(m.count, dtype=np.int64)
+                                     for m in sends]) if sends else np.zeros(0, np.int64)
+                if rows_l.size and (rows_l.min() < 0 or rows_l.max() >= nrows):
+                    raise AssertionError("partition: a sent row outside its color's rows")
+                order = np.argsort(rows_l, kind="stable")
+                ptr = np.zeros(nrows + 1, dtype=np.int64)
+                np.cumsum(np.bincount(rows_l, minlength=nrows), out=ptr[1:])
+                ex.push_row0 = row0
+                ex.push_ptr = ptr.astype(np.int32)
+                ex.push_rank = rk[order].astype(np.int32)
+                ex.push_off = ro[order].astype(np.int32)
+            return ex
 
         # the last forward phase and the last backward phase (color 0) feed
         # no later phase of their own sweep: no exchange after them

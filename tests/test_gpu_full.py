@@ -256,10 +256,11 @@ def test_split_pcg_full_config2(P, monkeypatch):
     _check_against_digest(rep, x, dg)
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32", "aniso12_b16_w32",
                                   "grid32_b8_w4"])
-def test_p2p_transport_sweeps_spmv_bitwise(P, name, world):
+def test_p2p_transport_sweeps_spmv_bitwise(P, name, world, fused):
     """NVLink-style transport (peer stores + release/acquire flags, no NCCL)
     with virtual ranks on one device: the pushes of every rank precede every
     wait in stream order, so no kernel ever waits on another rank's kernel."""
@@ -267,7 +268,7 @@ def test_p2p_transport_sweeps_spmv_bitwise(P, name, world):
     from paper_1908_00741_b200 import distributed
     g = load_golden(name)
     a, b, cfg, st, parts, ops, _ = _parts(P, name, world)
-    drv = distributed.DistHbmc(parts, ops, transport="p2p")
+    drv = distributed.DistHbmc(parts, ops, transport="p2p", fused=fused)
     n = st.layout.n_pad
     r = _scatter(ops, parts, g["r"])
     y = [drv.ext_vec(i, "y") for i in range(world)]
