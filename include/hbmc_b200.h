@@ -370,6 +370,10 @@ typedef struct {
 } tb_push_desc;
 int tb_plan_sweep_phase_push(tb_plan *plan, int forward, int64_t phase, const double *src,
                              double *dst, const tb_push_desc *push, void *stream);
+/* tb_dev_cg_p with the SpMV's p-halo push fused in (same desc semantics,
+ * rows [row0, row0 + nrows) of the rank's vector). */
+int tb_dev_cg_p_push(int64_t n, const double *s, int32_t num, int32_t den, const double *z,
+                     double *p, const tb_push_desc *push, void *stream);
 
 /* K/numba_backend.py:40-79 ic0_factor on the device, bitwise, for a system
  * in HBMC order (src/precond.py:179-200 with layout "hbmc"): one launch per

@@ -209,6 +209,50 @@ __global__ void wait_kernel(const unsigned *flags, int count, int skip, unsigned
 
 }  // namespace
 
+// p = z + beta p with the SpMV's halo push fused in: rows a peer needs are
+// stored into its p vector right after they are formed; the last CTA out
+// releases the epoch into every peer's flag for this rank.
+__global__ void __launch_bounds__(kT) p_push_kernel(long long n, const double *__restrict__ scal,
+                                                    int num, int den,
+                                                    const double *__restrict__ z,
+                                                    double *__restrict__ p, const tb_push_desc pd) {
+  const double beta = scal[num] / scal[den];
+  for (long long i = (long long)blockIdx.x * kT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kT) {
+    const double pi = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+    p[i] = pi;
+    const long long rel = i - pd.row0;
+    if (rel >= 0 && rel < pd.nrows)
+      for (int q = pd.ptr[rel]; q < pd.ptr[rel + 1]; ++q) pd.peer_dst[pd.peer[q]][pd.off[q]] = pi;
+  }
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(pd.done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    if (threadIdx.x == 0) *pd.done_ctr = 0;
+    __threadfence_system();
+    if (threadIdx.x < pd.npeers)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pd.peer_flag[threadIdx.x]),
+                   "r"(pd.epoch)
+                   : "memory");
+  }
+}
+
+extern "C" int tb_dev_cg_p_push(int64_t n, const double *scal, int32_t num, int32_t den,
+                                const double *z, double *p, const tb_push_desc *pd,
+                                void *stream) {
+  if (n < 0 || num < 0 || den < 0 || !pd || !pd->done_ctr || pd->npeers < 0 ||
+      pd->npeers > TB_MAX_PEERS)
+    return fail(TB_EINVAL, "dev_cg_p_push: bad arguments");
+  int g = grid_of(n);
+  if (g > 592) g = 592;
+  p_push_kernel<<<g, kT, 0, (cudaStream_t)stream>>>(n, scal, num, den, z, p, *pd);
+  CU(cudaGetLastError());
+  return TB_OK;
+}
+
 extern "C" int tb_p2p_alloc(int64_t bytes, void **ptr, void *handle64) {
   *ptr = nullptr;
   if (bytes <= 0) return fail(TB_EINVAL, "p2p_alloc: bytes <= 0");

@@ -270,6 +270,30 @@ class P2PTransport:
             _lib.check(_lib.LIB.tb_p2p_wait(self.bufs[i]["flags"][0], self.world, p.rank,
                                             self.epoch, st))
 
+    def fused_p_update(self, scal, num, den, z, p):
+        """p = z + beta p on every local rank with the p-halo push fused in;
+        returns the epoch the next SpMV waits for."""
+        import ctypes as C
+        from . import device as D
+        self.epoch = (self.epoch + 1) & 0x7fffffff
+        st = D.current_stream()
+        for i, part in enumerate(self.drv.parts):
+            ex = part.spmv
+            desc = self._desc(i, "spmv", -1, "p", ex)
+            desc.epoch = self.epoch
+            _lib.check(_lib.LIB.tb_dev_cg_p_push(part.n_loc, _lib.ptr(scal[i]), num, den,
+                                                 _lib.ptr(z[i]), _lib.ptr(p[i]),
+                                                 C.byref(desc), st))
+            self.drv.bytes_sent += 8 * int(ex.push_off.shape[0])
+        return self.epoch
+
+    def wait(self, epoch):
+        from . import device as D
+        st = D.current_stream()
+        for i, p in enumerate(self.drv.parts):
+            _lib.check(_lib.LIB.tb_p2p_wait(self.bufs[i]["flags"][0], self.world, p.rank,
+                                            epoch, st))
+
     def vec(self, i, name):
         return self.bufs[i][name][1][: self.drv.parts[i].n_ext]
 
@@ -342,6 +366,7 @@ class DistHbmc:
         self.exchanges = 0
         self.bytes_sent = 0
         self.p2p = P2PTransport(self, fused=fused) if transport == "p2p" else None
+        self._p_epoch = 0
 
     @staticmethod
     def _ex(p, kind, c):
@@ -444,9 +469,23 @@ class DistHbmc:
         self.sweep(False, y, z)
 
     def spmv(self, x, out):
-        self.exchange("spmv", -1, x)
+        if self._p_epoch:   # the p update already pushed the halo: just wait
+            self.p2p.wait(self._p_epoch)
+            self._p_epoch = 0
+            self.exchanges += 1
+        else:
+            self.exchange("spmv", -1, x)
         for i in range(len(self.parts)):
             self.ops[i].spmv(x[i], out[i])
+
+    def update_p(self, sc, num, den, z, p):
+        """p = z + beta p; with the fused P2P transport the p halo for the next
+        SpMV is pushed by the same kernel."""
+        if self.p2p is not None and self.p2p.fused and all(o.plan is not None for o in self.ops):
+            self._p_epoch = self.p2p.fused_p_update(sc, num, den, z, p)
+            return
+        for i in range(len(self.parts)):
+            self.ops[i].update_p(sc[i], num, den, z[i], p[i])
 
     # ---------------------------------------------------------------- PCG
     def pcg(self, b_loc, tol=1e-7, max_iters=50000):
@@ -457,6 +496,7 @@ class DistHbmc:
         """
         R = range(len(self.parts))
         O = self.ops
+        self._p_epoch = 0   # a halo push left over from an earlier solve is stale
         V = lambda name: [self.ext_vec(i, name) for i in R]  # noqa: E731
         x, r, y, z, p, ap = V("x"), V("r"), V("y"), V("z"), V("p"), V("ap")
         sc = [O[i].scalars() for i in R]
@@ -498,8 +538,7 @@ class DistHbmc:
             for i in R:
                 O[i].dot(r[i], z[i], sc[i], rzn)
             self.allreduce(sc, [rzn])
-            for i in R:
-                O[i].update_p(sc[i], rzn, rz, z[i], p[i])
+            self.update_p(sc, rzn, rz, z, p)
             rz, rzn = rzn, rz
         return x, it, history, converged
 

@@ -261,10 +261,10 @@ def partition_hbmc(L, U, A, inv_d, color_lvl1_ranges, b_s, w, world, ranks=None)
                     recvs.append(Msg(s, n_loc + a, b - a))
             idx = (np.concatenate(send_idx) if send_idx else np.zeros(0, np.int64))
             ex = Exchange(idx.astype(np.int32), sends, recvs)
-            if kind != "spmv":
-                # rows of color c on this rank: [row0, row0 + nrows)
-                row0 = int(lcr_[c]) * span
-                nrows = int(lcr_[c + 1] - lcr_[c]) * span
+            if True:
+                # rows the push may come from: color c's (sweeps) or all (spmv)
+                row0 = 0 if kind == "spmv" else int(lcr_[c]) * span
+                nrows = n_loc if kind == "spmv" else int(lcr_[c + 1] - lcr_[c]) * span
                 rows_l = idx.astype(np.int64) - row0
                 rk = np.concatenate([np.full(m.count, m.peer, np.int64) for m in sends]) \
                     if sends else np.zeros(0, np.int64)

@@ -293,6 +293,26 @@ def test_p2p_transport_sweeps_spmv_bitwise(P, name, world, fused):
         o.close()
 
 
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32", "aniso12_b16_w32"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_fused_pcg_on_device(P, name, world):
+    """Partitioned PCG with the fused P2P transport (sweep kernels and the p
+    update store the halos themselves), virtual ranks, twice on one driver."""
+    from paper_1908_00741_b200 import distributed
+    g = load_golden(name)
+    a, b, cfg, st, parts, ops, _ = _parts(P, name, world)
+    drv = distributed.DistHbmc(parts, ops, transport="p2p")
+    for _ in range(2):
+        xs, it, hist, conv = drv.pcg([o.from_host(st.b_sys[p.rows]) for o, p in zip(ops, parts)],
+                                     cfg.tol, cfg.max_iters)
+        x = _gather(ops, parts, xs, st.layout.n_pad)[st.old_positions]
+        assert abs(it - int(g["pcg_hbmc_iters"])) <= 1
+        assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
+    drv.close()
+    for o in ops:
+        o.close()
+
+
 def test_p2p_transport_pcg_full_config2(P):
     from paper_1908_00741_b200 import distributed, problems
     dg = _digest(2)
