@@ -1623,6 +1623,12 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
     }
   }
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
+  // Without the dataflow schedule a small system runs faster as per-phase
+  // kernels in a CUDA graph (config 1: ICCG 2.01 vs 2.44 ms, precond 36 vs
+  // 61 us); large barrier-mode systems keep the single launch (config 4:
+  // 165.5 vs 170.7 ms).
+  if (pl->n_lvl1_flow == 0 && pl->n < (long long)env_int("TB_PERSIST_MIN_N", 1 << 20))
+    pl->persist_ok = false;
   if (env_int("TB_TRACE", 0)) {
     CU(cudaMalloc((void **)&pl->trace, 64 * sizeof(unsigned long long)));
     CU(cudaMemset(pl->trace, 0, 64 * sizeof(unsigned long long)));
