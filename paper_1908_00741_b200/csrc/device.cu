@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(kBlock)
   }
 
 // x += alpha p; r -= alpha ap; rel = ||r|| / ||b|| (src/solver.py:178-186).
+template <bool PAIRS = false>
 __global__ void __launch_bounds__(kBlock)
     cg_update_xr(long long n, const double *__restrict__ p,
                  const double *__restrict__ ap, double *__restrict__ x,
@@ -376,12 +377,28 @@ __global__ void __launch_bounds__(kBlock)
   if (st->done) return;
   const double alpha = st->alpha;
   double part = 0.0;
-  TB_GRID_STRIDE4({
-    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
-    const double ri = __dsub_rn(r[i], __dmul_rn(alpha, ap[i]));
-    r[i] = ri;
-    part += ri * ri;
-  })
+  if (PAIRS) {   // 16-byte accesses (n even)
+    TB_PAIRS4({
+      const double2 xo = *(const double2 *)(x + i), po = *(const double2 *)(p + i);
+      const double2 ro = *(const double2 *)(r + i), ao = *(const double2 *)(ap + i);
+      double2 xn, rn;
+      xn.x = __dadd_rn(xo.x, __dmul_rn(alpha, po.x));
+      xn.y = __dadd_rn(xo.y, __dmul_rn(alpha, po.y));
+      rn.x = __dsub_rn(ro.x, __dmul_rn(alpha, ao.x));
+      rn.y = __dsub_rn(ro.y, __dmul_rn(alpha, ao.y));
+      *(double2 *)(x + i) = xn;
+      *(double2 *)(r + i) = rn;
+      part += rn.x * rn.x;
+      part += rn.y * rn.y;
+    })
+  } else {
+    TB_GRID_STRIDE4({
+      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+      const double ri = __dsub_rn(r[i], __dmul_rn(alpha, ap[i]));
+      r[i] = ri;
+      part += ri * ri;
+    })
+  }
   grid_reduce(part, partials, &st->counter[2], [st, hist](double rr) {
     const long long j = st->iter + 1;
     const double rel = sqrt(rr) / st->bnorm;
@@ -499,18 +516,27 @@ __global__ void __launch_bounds__(spmv_tma::kThreads, 2)
 
 // rz_new = r . z; beta = rz_new / rz; rz = rz_new (src/solver.py:190-192).
 // FIRST: the prologue's rz = r . z and p = z.
-template <bool FIRST>
+template <bool FIRST, bool PAIRS = false>
 __global__ void __launch_bounds__(kBlock)
     cg_rz(long long n, const double *__restrict__ r,
           const double *__restrict__ z, double *__restrict__ p,
           double *partials, PcgState *st) {
   if (st->done) return;
   double part = 0.0;
-  TB_GRID_STRIDE4({
-    const double zi = z[i];
-    part += r[i] * zi;
-    if (FIRST) p[i] = zi;
-  })
+  if (PAIRS) {
+    TB_PAIRS4({
+      const double2 zi = *(const double2 *)(z + i), ri = *(const double2 *)(r + i);
+      part += ri.x * zi.x;
+      part += ri.y * zi.y;
+      if (FIRST) *(double2 *)(p + i) = zi;
+    })
+  } else {
+    TB_GRID_STRIDE4({
+      const double zi = z[i];
+      part += r[i] * zi;
+      if (FIRST) p[i] = zi;
+    })
+  }
   grid_reduce(part, partials, &st->counter[3], [st](double rz) {
     if (FIRST) {
       st->rz = rz;
@@ -522,12 +548,23 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // p = z + beta p (src/solver.py:193).
+template <bool PAIRS = false>
 __global__ void __launch_bounds__(kBlock)
     cg_update_p(long long n, const double *__restrict__ z,
                 double *__restrict__ p, const PcgState *st) {
   if (st->done) return;
   const double beta = st->beta;
-  TB_GRID_STRIDE4({ p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i])); })
+  if (PAIRS) {
+    TB_PAIRS4({
+      const double2 zi = *(const double2 *)(z + i), po = *(const double2 *)(p + i);
+      double2 pn;
+      pn.x = __dadd_rn(zi.x, __dmul_rn(beta, po.x));
+      pn.y = __dadd_rn(zi.y, __dmul_rn(beta, po.y));
+      *(double2 *)(p + i) = pn;
+    })
+  } else {
+    TB_GRID_STRIDE4({ p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i])); })
+  }
 }
 
 // Next preconditioner epoch for graph-replayed dataflow launches.
@@ -1378,16 +1415,20 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   } else {
     if ((rc = launch_spmv(pl, pl->p, pl->ap, s, true, nl))) return rc;
     if ((rc = debug_sync(pl, s, "spmv+dot"))) return rc;
-    cg_update_xr<<<rg, kBlock, 0, s>>>(n, pl->p, pl->ap, x, pl->r, pl->partials,
-                                       pl->st, pl->hist);
+    const bool pairs = (n % 2) == 0 && env_int("TB_VEC_PAIRS", 1);
+    (pairs ? cg_update_xr<true> : cg_update_xr<false>)<<<rg, kBlock, 0, s>>>(
+        n, pl->p, pl->ap, x, pl->r, pl->partials, pl->st, pl->hist);
     ++*nl;
     if ((rc = debug_sync(pl, s, "cg_update_xr"))) return rc;
   }
   if ((rc = launch_precond_step(pl, s, nl))) return rc;
   if ((rc = debug_sync(pl, s, "precond"))) return rc;
-  cg_rz<false><<<rg, kBlock, 0, s>>>(n, pl->r, pl->z, pl->p, pl->partials, pl->st);
+  const bool pairs2 = (n % 2) == 0 && env_int("TB_VEC_PAIRS", 1);
+  (pairs2 ? cg_rz<false, true> : cg_rz<false, false>)<<<rg, kBlock, 0, s>>>(
+      n, pl->r, pl->z, pl->p, pl->partials, pl->st);
   if ((rc = debug_sync(pl, s, "cg_rz"))) return rc;
-  cg_update_p<<<reduce_grid(n, pl->vec_pt), kBlock, 0, s>>>(n, pl->z, pl->p, pl->st);
+  (pairs2 ? cg_update_p<true> : cg_update_p<false>)<<<reduce_grid(n, pl->vec_pt), kBlock, 0, s>>>(
+      n, pl->z, pl->p, pl->st);
   *nl += 2;
   if ((rc = debug_sync(pl, s, "cg_update_p"))) return rc;
   CU(cudaGetLastError());
