@@ -24,6 +24,9 @@
 
 #include "sweep_lean.cuh"
 
+#ifndef TB_FLAG_NS
+#define TB_FLAG_NS 0   // back-off between dependency-flag polls (ns), 0 = spin
+#endif
 #ifndef TB_SMALL_DEPTH
 #define TB_SMALL_DEPTH 2
 #endif
@@ -216,8 +219,10 @@ __device__ __forceinline__ void wait_flags(const Params &P, const unsigned *flag
     const unsigned *f = flags + dep[q];
     if (ld_relaxed(f) < epoch) {
       const long long t0 = clock64();
-      while (ld_relaxed(f) < epoch)
+      while (ld_relaxed(f) < epoch) {
+        if (TB_FLAG_NS > 0) __nanosleep(TB_FLAG_NS);
         if (clock64() - t0 > P.watchdog) __trap();
+      }
     }
   }
   __syncwarp();
