@@ -514,6 +514,39 @@ __global__ void __launch_bounds__(spmv_tma::kThreads, 2)
   }
 }
 
+// r . z, beta and p = z + beta p in ONE cooperative launch (src/solver.py:
+// 190-193), 16-byte accesses, n even: the deterministic grid sum (CTA
+// partials added in index order by every CTA after a grid barrier) replaces
+// cg_rz's last-CTA reduction, and the p update follows without a second
+// launch.  Every CTA reads the old rz before the barrier; CTA 0 publishes
+// the new rz / beta after it.
+__global__ void __launch_bounds__(kBlock)
+    cg_rz_p_coop(long long n, const double *__restrict__ r, const double *__restrict__ z,
+                 double *__restrict__ p, double *partials, unsigned *bar, PcgState *st) {
+  __shared__ double sh[33];
+  if (st->done) return;
+  const double rz_old = st->rz;
+  double part = 0.0;
+  TB_PAIRS4({
+    const double2 zi = *(const double2 *)(z + i), ri = *(const double2 *)(r + i);
+    part += ri.x * zi.x;
+    part += ri.y * zi.y;
+  })
+  const double rzn = coop_sum(part, partials, bar, sh);
+  const double beta = rzn / rz_old;
+  TB_PAIRS4({
+    const double2 zi = *(const double2 *)(z + i), po = *(const double2 *)(p + i);
+    double2 pn;
+    pn.x = __dadd_rn(zi.x, __dmul_rn(beta, po.x));
+    pn.y = __dadd_rn(zi.y, __dmul_rn(beta, po.y));
+    *(double2 *)(p + i) = pn;
+  })
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->beta = beta;
+    st->rz = rzn;
+  }
+}
+
 // rz_new = r . z; beta = rz_new / rz; rz = rz_new (src/solver.py:190-192).
 // FIRST: the prologue's rz = r . z and p = z.
 template <bool FIRST, bool PAIRS = false>
@@ -957,6 +990,7 @@ struct tb_plan {
   bool split_pcg = false;
   int vec_pt = 16;             // elements per thread of the CG vector kernels (grid size)
   int xr_grid = 0;             // spmv_tma_xr cooperative grid (0 = separate x/r pass)
+  int rzp_grid = 0;            // cg_rz_p_coop cooperative grid (0 = cg_rz + cg_update_p)
   bool in_graph = false;       // capturing the split graph: precond epochs from epoch_dev
   bool g_split = false;        // the instantiated graph is the split variant
   unsigned *epoch_dev = nullptr;
@@ -1424,11 +1458,23 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   if ((rc = launch_precond_step(pl, s, nl))) return rc;
   if ((rc = debug_sync(pl, s, "precond"))) return rc;
   const bool pairs2 = (n % 2) == 0 && env_int("TB_VEC_PAIRS", 1);
-  (pairs2 ? cg_rz<false, true> : cg_rz<false, false>)<<<rg, kBlock, 0, s>>>(
-      n, pl->r, pl->z, pl->p, pl->partials, pl->st);
-  if ((rc = debug_sync(pl, s, "cg_rz"))) return rc;
-  (pairs2 ? cg_update_p<true> : cg_update_p<false>)<<<reduce_grid(n, pl->vec_pt), kBlock, 0, s>>>(
-      n, pl->z, pl->p, pl->st);
+  if (pairs2 && pl->rzp_grid > 0 && pl->bar) {
+    long long nn = n;
+    const double *rr = pl->r, *zz = pl->z;
+    double *pp = pl->p, *pa = pl->partials;
+    unsigned *bb = pl->bar;
+    PcgState *ss = pl->st;
+    void *args[] = {&nn, &rr, &zz, &pp, &pa, &bb, &ss};
+    CU(cudaLaunchCooperativeKernel((const void *)cg_rz_p_coop, dim3(pl->rzp_grid),
+                                   dim3(kBlock), args, 0, s));
+    --*nl;   // one launch instead of two
+  } else {
+    (pairs2 ? cg_rz<false, true> : cg_rz<false, false>)<<<rg, kBlock, 0, s>>>(
+        n, pl->r, pl->z, pl->p, pl->partials, pl->st);
+    if ((rc = debug_sync(pl, s, "cg_rz"))) return rc;
+    (pairs2 ? cg_update_p<true> : cg_update_p<false>)<<<reduce_grid(n, pl->vec_pt), kBlock, 0, s>>>(
+        n, pl->z, pl->p, pl->st);
+  }
   *nl += 2;
   if ((rc = debug_sync(pl, s, "cg_update_p"))) return rc;
   CU(cudaGetLastError());
@@ -1664,6 +1710,14 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
     }
   }
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
+  if (env_int("TB_RZP_FUSE", 1)) {   // fused r.z + p update for the kernel-sequence paths
+    int ps = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cg_rz_p_coop, kBlock, 0));
+    const long long want = ((pl->n + 1) / 2 + kBlock * 8 - 1) / (kBlock * 8);  // ~16 elements/thread
+    long long g = (long long)ps * pl->num_sms;
+    if (want < g) g = want;
+    pl->rzp_grid = g > 0 ? (int)g : 0;
+  }
   // Without the dataflow schedule a small system runs faster as per-phase
   // kernels in a CUDA graph (config 1: ICCG 2.01 vs 2.44 ms, precond 36 vs
   // 61 us); large barrier-mode systems keep the single launch (config 4:
