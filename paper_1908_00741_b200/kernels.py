@@ -119,8 +119,14 @@ def _dev_in(a):
     return device.to_device(_f64(a))
 
 
-def _dev_rw(a):
-    """(device tensor, writeback) for an in/out float64 array."""
+def _dev_rw(a, lo=0, hi=None):
+    """(device tensor, writeback) for an in/out float64 array.
+
+    Only rows [lo, hi) -- the ones the kernel writes -- are copied back: the
+    reference calls the range kernels from several WorkerPool threads at
+    once on disjoint ranges of one output array (src/precond.py:131-139), so
+    writing back the whole array would overwrite a concurrent call's rows
+    with this call's stale copy."""
     from . import device
     t = device.torch()
     if isinstance(a, t.Tensor) and a.is_cuda:
@@ -128,9 +134,11 @@ def _dev_rw(a):
     if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
         raise TypeError("output must be a C-contiguous float64 array (updated in place)")
     d = device.to_device(a)
+    hi = a.shape[0] if hi is None else hi
 
     def writeback():
-        a[:] = d.cpu().numpy()
+        if hi > lo:
+            a[lo:hi] = d[lo:hi].cpu().numpy()
     return d, writeback
 
 
@@ -173,7 +181,7 @@ def _csr_range(forward, rp, ci, vals, inv_d, src, dst, start, end):
     vd = _dev_ro(vals, np.float64)
     idd = _dev_ro(inv_d, np.float64)
     sd = _dev_in(src)
-    dd, wb = _dev_rw(dst)
+    dd, wb = _dev_rw(dst, int(start), int(end))
     # the range is one sequential task (rows ascending / descending)
     tpd = _dev_in(np.array([int(start), int(end)], dtype=np.float64)).to(
         dtype=__import__("torch").int64)
@@ -202,7 +210,8 @@ def _sell_range(forward, slice_ptr, slice_len, col_idx, vals, inv_d, src, dst, w
     vd = _dev_ro(vals, np.float64)
     idd = _dev_ro(inv_d, np.float64)
     sd = _dev_in(src)
-    dd, wb = _dev_rw(dst)
+    rows_per_block = int(width) * int(block_rows)
+    dd, wb = _dev_rw(dst, int(k0) * rows_per_block, int(k1) * rows_per_block)
     fn = LIB.tb_dev_fwd_sell_range if forward else LIB.tb_dev_bwd_sell_range
     check(fn(ptr(sp), ptr(sl), ptr(ci), ptr(vd), ptr(idd), ptr(sd), ptr(dd), int(width),
              int(block_rows), int(k0), int(k1), _stream()))

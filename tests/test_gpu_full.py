@@ -364,3 +364,32 @@ def test_pcg_paths_interleaved_on_one_plan(P, monkeypatch):
         out.append(x)
     assert np.array_equal(out[0], out[3])     # graph replay is deterministic
     st.plan.close()
+
+
+def test_kernel_seam_concurrent_ranges(P):
+    """The reference calls the range kernels from several WorkerPool threads
+    at once on disjoint ranges of one output array (src/precond.py:131-139):
+    the seam must not clobber another call's rows (found by running the
+    reference's own suite through this seam)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1908_00741_b200 import kernels, precond
+    a, b = P.gen_laplacian_5pt(48, 48)
+    col = P.greedy_color_nodes(a)
+    a_o, _ = P.permute_system(a, b, col.perm)
+    f = P.ic0_factorize(a_o, layout_tag="mc")
+    r = np.random.default_rng(3).standard_normal(a.n)
+    y_ref = np.empty(a.n)
+    kernels.fwd_csr_range(f.L.row_ptr, f.L.col_idx, f.L.vals, f.inv_diag, r, y_ref, 0, a.n)
+    ranges = col.color_ranges if hasattr(col, "color_ranges") else None
+    bounds = np.asarray(ranges) if ranges is not None else np.array([0, a.n])
+    y = np.full(a.n, np.nan)
+    for c in range(bounds.shape[0] - 1):
+        lo, hi = int(bounds[c]), int(bounds[c + 1])
+        chunks = [(lo + (hi - lo) * i // 8, lo + (hi - lo) * (i + 1) // 8) for i in range(8)]
+        with ThreadPoolExecutor(8) as ex:
+            list(ex.map(lambda se: kernels.fwd_csr_range(f.L.row_ptr, f.L.col_idx, f.L.vals,
+                                                          f.inv_diag, r, y, se[0], se[1]),
+                        chunks))
+    assert np.array_equal(y, y_ref)
+    del precond
