@@ -230,3 +230,23 @@ def fwd_sell_range(slice_ptr, slice_len, col_idx, vals, inv_d, r, y, width, bloc
 def bwd_sell_range(slice_ptr, slice_len, col_idx, vals, inv_d, y, z, width, block_rows, k0, k1):
     """K/numba_backend.py:156-171 (z in place)."""
     _sell_range(False, slice_ptr, slice_len, col_idx, vals, inv_d, y, z, width, block_rows, k0, k1)
+
+
+# ------------------------------------------------------------ registry
+# src/_kernels/__init__.py:46-73 resolves a backend name to a kernel module.
+# This package has exactly one backend (the B200 one; no multi-backend
+# dispatch), so the registry has one entry.
+def available_backends():
+    return [NAME]
+
+
+def default_backend():
+    return NAME
+
+
+def get_kernels(backend=None):
+    """The kernel module for `backend` (None / "auto" / "cuda": this one)."""
+    import sys
+    if backend in (None, "auto", NAME):
+        return sys.modules[__name__]
+    raise ValueError(f"unknown backend {backend!r}; available: {available_backends()}")
