@@ -154,6 +154,19 @@ int tb_mm_entries(const char *buf, int64_t len, int64_t body_pos, int64_t first_
                   int64_t *found, int64_t *kth_line, int32_t *err_kind, int64_t *err_line,
                   int64_t *err_b, int64_t *err_e);
 
+/* Setup helpers on a CSR pattern with sorted columns (host, OpenMP):
+ * diagonal slot per row (-1 if none); structural symmetry; strictly lower
+ * (upper = 0) / upper (upper = 1) part: count pass then fill pass. */
+int tb_csr_diag_ptr(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                    int64_t *diag_out);
+int tb_csr_is_symmetric(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                        int32_t *symmetric);
+int tb_csr_tri_count(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int32_t upper,
+                     int64_t *row_out);
+int tb_csr_tri_fill(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                    const double *vals, int32_t upper, const int64_t *row_out,
+                    int64_t *col_out, double *val_out);
+
 /* =========================================================================
  * Device operators on caller-owned device buffers (e.g. torch.cuda tensors
  * passed as data_ptr()).  `stream` is a cudaStream_t (NULL = legacy default).

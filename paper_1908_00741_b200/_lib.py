@@ -120,6 +120,10 @@ _SIGS = {
     "tb_dev_cg_p": [i64, vp, i32, i32, vp, vp, vp],
     "tb_plan_sweep_phase_push": [vp, C.c_int, i64, vp, vp, C.POINTER(TbPushDesc), vp],
     "tb_dev_cg_p_push": [i64, vp, i32, i32, vp, vp, C.POINTER(TbPushDesc), vp],
+    "tb_csr_diag_ptr": [i64, vp, vp, vp],
+    "tb_csr_is_symmetric": [i64, vp, vp, C.POINTER(i32)],
+    "tb_csr_tri_count": [i64, vp, vp, i32, vp],
+    "tb_csr_tri_fill": [i64, vp, vp, vp, i32, vp, vp, vp],
     "tb_p2p_alloc": [i64, C.POINTER(vp), vp],
     "tb_p2p_free": [vp],
     "tb_p2p_open": [vp, C.POINTER(vp)],

@@ -470,6 +470,80 @@ extern "C" int tb_csr_transpose(int64_t n, const int64_t *row_ptr,
   TB_TRY_END
 }
 
+// Setup helpers over a CSR pattern with sorted columns (OpenMP over rows):
+// the diagonal slot of every row (-1 if absent), whether the pattern is
+// structurally symmetric (every (i, j) has (j, i)), and the strictly lower
+// / upper part as a new CSR (src/precond.py:163-169).  The numpy versions
+// allocate nnz-sized temporaries several times; at config 5 (938M entries)
+// these three dominated the host setup.
+extern "C" int tb_csr_diag_ptr(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                               int64_t *diag_out) {
+  if (n < 0) return fail(TB_EINVAL, "csr_diag_ptr: bad arguments");
+#pragma omp parallel for schedule(static, 4096)
+  for (int64_t i = 0; i < n; ++i) {   // linear scan: columns need not be sorted
+    int64_t d = -1;
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+      if (col_idx[p] == i) {
+        d = p;
+        break;
+      }
+    diag_out[i] = d;
+  }
+  return TB_OK;
+}
+
+extern "C" int tb_csr_is_symmetric(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                                   int32_t *symmetric) {
+  if (n < 0) return fail(TB_EINVAL, "csr_is_symmetric: bad arguments");
+  int bad = 0;
+#pragma omp parallel for schedule(static, 4096) reduction(| : bad)
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1] && !bad; ++p) {
+      const int64_t j = col_idx[p];
+      if (j < 0 || j >= n) { bad = 1; break; }
+      const int64_t *b = col_idx + row_ptr[j], *e = col_idx + row_ptr[j + 1];
+      const int64_t *q = std::lower_bound(b, e, i);
+      if (q == e || *q != i) bad = 1;
+    }
+  }
+  *symmetric = bad ? 0 : 1;
+  return TB_OK;
+}
+
+// upper = 0: strictly lower part; 1: strictly upper.  row_out [n+1]; the
+// caller sizes col_out / val_out with tb_csr_tri_count.
+extern "C" int tb_csr_tri_count(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                                int32_t upper, int64_t *row_out) {
+  if (n < 0) return fail(TB_EINVAL, "csr_tri_count: bad arguments");
+  row_out[0] = 0;
+#pragma omp parallel for schedule(static, 4096)
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t c = 0;
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+      c += upper ? (col_idx[p] > i) : (col_idx[p] < i);
+    row_out[i + 1] = c;
+  }
+  for (int64_t i = 0; i < n; ++i) row_out[i + 1] += row_out[i];
+  return TB_OK;
+}
+
+extern "C" int tb_csr_tri_fill(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                               const double *vals, int32_t upper, const int64_t *row_out,
+                               int64_t *col_out, double *val_out) {
+  if (n < 0) return fail(TB_EINVAL, "csr_tri_fill: bad arguments");
+#pragma omp parallel for schedule(static, 4096)
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t d = row_out[i];
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+      if (upper ? (col_idx[p] > i) : (col_idx[p] < i)) {
+        col_out[d] = col_idx[p];
+        val_out[d] = vals[p];
+        ++d;
+      }
+  }
+  return TB_OK;
+}
+
 // src/matrix.py:239-261 csr_to_sell fill: entry t of row i at
 // slice_ptr[i / w] + (i % w) + w * t; padding = (own row, 0.0).
 extern "C" int tb_csr_to_sell_fill(int64_t n, const int64_t *row_ptr,

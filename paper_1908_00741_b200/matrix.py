@@ -37,10 +37,9 @@ class CooMatrix:
 
 
 def _find_diag_ptr(n, row_ptr, col_idx):
-    diag_ptr = np.full(n, -1, dtype=np.int64)
-    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(row_ptr))
-    hits = np.nonzero(col_idx == rows)[0]
-    diag_ptr[rows[hits]] = hits
+    """Diagonal slot of every row, -1 if absent (native scan, host builder)."""
+    diag_ptr = np.empty(n, dtype=np.int64)
+    check(LIB.tb_csr_diag_ptr(n, ptr(row_ptr), ptr(col_idx), ptr(diag_ptr)))
     return diag_ptr
 
 

@@ -132,18 +132,22 @@ class WorkerPool:
 
 
 def _strict_tri(a: CsrMatrix, upper=False):
-    rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.row_ptr))
-    mask = (a.col_idx > rows) if upper else (a.col_idx < rows)
-    row_ptr = np.zeros(a.n + 1, dtype=np.int64)
-    np.cumsum(np.bincount(rows[mask], minlength=a.n), out=row_ptr[1:])
-    return CsrMatrix(a.n, row_ptr, a.col_idx[mask], a.vals[mask],
-                     diag_ptr=np.full(a.n, -1, dtype=np.int64))
+    """src/precond.py:163-169: strictly lower (upper) part, native two-pass."""
+    row_ptr = np.empty(a.n + 1, dtype=np.int64)
+    check(LIB.tb_csr_tri_count(a.n, ptr(a.row_ptr), ptr(a.col_idx), 1 if upper else 0,
+                               ptr(row_ptr)))
+    nnz = int(row_ptr[-1])
+    col = np.empty(nnz, dtype=np.int64)
+    val = np.empty(nnz, dtype=np.float64)
+    check(LIB.tb_csr_tri_fill(a.n, ptr(a.row_ptr), ptr(a.col_idx), ptr(a.vals),
+                              1 if upper else 0, ptr(row_ptr), ptr(col), ptr(val)))
+    return CsrMatrix(a.n, row_ptr, col, val, diag_ptr=np.full(a.n, -1, dtype=np.int64))
 
 
 def _check_structural_symmetry(a: CsrMatrix):
-    at = csr_transpose(a)
-    if not (np.array_equal(at.row_ptr, a.row_ptr)
-            and np.array_equal(at.col_idx, a.col_idx)):
+    ok = _lib.i32()
+    check(LIB.tb_csr_is_symmetric(a.n, ptr(a.row_ptr), ptr(a.col_idx), ok))
+    if not ok.value:
         raise ValueError("matrix structure is not symmetric")
 
 
