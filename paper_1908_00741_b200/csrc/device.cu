@@ -1844,6 +1844,7 @@ int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
   // padding and the scattered gathers dominate -- the thread-per-row kernel
   // measured faster there (profiles/README.md).
   long long pad = 0;
+#pragma omp parallel for schedule(static, 1024) reduction(+ : pad)
   for (long long s = 0; s < h.n_slices; ++s) {
     const long long off = h.slice_ptr[s];
     for (long long q = off; q < off + (long long)h.slice_len[s] * 32; ++q)
