@@ -393,3 +393,28 @@ def test_kernel_seam_concurrent_ranges(P):
                         chunks))
     assert np.array_equal(y, y_ref)
     del precond
+
+
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32", "s27_10_b8_w32",
+                                  "aniso12_b16_w32", "lap7_12_b4_w8"])
+@pytest.mark.parametrize("env", [{}, {"TB_DATAFLOW": "0"}, {"TB_PERSIST": "0"},
+                                 {"TB_PERSIST": "0", "TB_SWEEP": "simple"},
+                                 {"TB_PERSIST_MIN_N": "0"}, {"TB_FLOW_MAXDEP": "0"}])
+def test_every_precond_path_bitwise(P, name, env, monkeypatch):
+    """Every internal schedule of the preconditioner (dataflow persistent,
+    barrier persistent, per-phase lean / simple kernels) gives the
+    reference's z bit for bit."""
+    import torch
+    from paper_1908_00741_b200 import solver
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = load_golden(name)
+    a, bs, w, _ = golden_matrix(name)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    st = solver.attach_plan(solver.prepare(a, np.zeros(a.n), cfg), cfg)
+    r = torch.from_numpy(np.ascontiguousarray(g["r"])).cuda()
+    z = torch.full_like(r, float("nan"))
+    st.plan.precond(r, z)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.cpu().numpy(), g["z"])
+    st.plan.close()
