@@ -418,3 +418,26 @@ def test_every_precond_path_bitwise(P, name, env, monkeypatch):
     torch.cuda.synchronize()
     assert np.array_equal(z.cpu().numpy(), g["z"])
     st.plan.close()
+
+
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "aniso12_b16_w32", "lap7_12_b4_w8"])
+@pytest.mark.parametrize("env", [{}, {"TB_PCG_SPLIT": "0"}, {"TB_PCG_SPLIT_POLL": "2"},
+                                 {"TB_PERSIST": "0"}, {"TB_PCG_NOGRAPH": "3"},
+                                 {"TB_RZP_FUSE": "0"}, {"TB_VEC_PAIRS": "0"},
+                                 {"TB_SPMV_TMA": "0"}])
+def test_every_pcg_path_meets_the_bar(P, name, env, monkeypatch):
+    """Every tb_pcg execution path (split graph / host-polled, single
+    persistent launch, per-phase graph, host-polled kernel sequence, with
+    and without the fused / paired vector kernels and the TMA SpMV) meets
+    the north-star bar against the reference's run."""
+    from paper_1908_00741_b200 import problems
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = load_golden(name)
+    a, bs, w, _ = golden_matrix(name)
+    _, b = problems.rhs(a)
+    x, rep = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell"))
+    assert rep.converged == bool(g["pcg_hbmc_converged"])
+    assert abs(rep.iterations - int(g["pcg_hbmc_iters"])) <= 1
+    assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
+    assert rep.barrier_total == int(g["pcg_hbmc_barriers"])
