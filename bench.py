@@ -345,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
     # vectors (H2D of step i+1 and D2H of step i-1 overlap step i's sweeps;
     # PCIe is full duplex), as a caller streaming right-hand sides would run
     # it.  Timed from the first H2D to the last D2H on the device.
-    nbuf = 2
+    nbuf = int(os.environ.get("TB_E2E_NBUF", "2"))
     r_host = torch.from_numpy(np.random.default_rng(0).standard_normal(n_pad)).pin_memory()
     z_host = [torch.empty(n_pad, dtype=torch.float64).pin_memory() for _ in range(nbuf)]
     r_dev = [torch.empty(n_pad, dtype=torch.float64, device=dev) for _ in range(nbuf)]
@@ -455,7 +455,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_pad, "d2h_bytes_per_step": 8 * n_pad,
                     "ms_per_step": e2e_ms_max / args.steps,
-                    "pipeline": "H2D / precond / D2H on 3 streams, 2 device buffers"},
+                    "pipeline": f"H2D / precond / D2H on 3 streams, {nbuf} device buffers"},
             "gpu_launches": args.steps if pinfo["precond"] else launches,
             "clocks": clk.summary(),
             "iccg": {"iterations": int(rep.iterations),
