@@ -1865,9 +1865,10 @@ int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
   // candidates (slices per chunk, stages, smem budget KB) in order of
   // preference, from the A/B in profiles/README.md: 16 slices (two per warp,
   // 16 gathers in flight per lane) x 2 stages at 2 CTAs/SM for short rows;
-  // one 16-slice stage at 1 CTA/SM for long rows (27-point)
+  // one 8-slice stage at 2 CTAs/SM for long rows (27-point: 585 us vs 638
+  // with one 16-slice stage at 1 CTA/SM)
   struct Cand { int S, D, kb; };
-  Cand cands[3] = {{16, 2, 100}, {16, 1, 220}, {0, 0, 0}};
+  Cand cands[4] = {{16, 2, 100}, {8, 1, 100}, {16, 1, 220}, {0, 0, 0}};
   if (env_int("TB_SPMV_S", 0) > 0)
     cands[0] = {env_int("TB_SPMV_S", 16), env_int("TB_SPMV_D", 2), env_int("TB_SPMV_KB", 100)},
     cands[1] = {0, 0, 0};
@@ -2234,10 +2235,11 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
   {
     const int se = env_int("TB_PCG_SPLIT", -1);
     const long long sn = (long long)env_int("TB_PCG_SPLIT_N", kSplitN);
-    // default only with the double-buffered TMA SpMV (short rows: configs
-    // 1, 2, 5); long rows (27-point) measured faster in the single launch
+    // default whenever the TMA SpMV and the dataflow precond apply
+    // (configs 2, 3, 5: 23.3 / 51.9 / 1694 ms vs 28.5 / 54.4 / ~2000 ms for
+    // the single persistent launch)
     pl->split_pcg = pl->persist_ok && pl->n_lvl1_flow > 0 && pl->spmv_S > 0 &&
-                    (se == 1 || (se < 0 && pl->n >= sn && pl->spmv_D >= 2));
+                    (se == 1 || (se < 0 && pl->n >= sn));
     // the split path runs as a CUDA graph (conditional WHILE, device-side
     // convergence test) unless TB_PCG_SPLIT_POLL=n asks for host polling
     if (pl->split_pcg && check_every <= 0) check_every = env_int("TB_PCG_SPLIT_POLL", 0);
