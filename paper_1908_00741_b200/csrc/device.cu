@@ -1850,8 +1850,9 @@ int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
     for (long long q = off; q < off + (long long)h.slice_len[s] * 32; ++q)
       pad += h.vals[q] == 0.0 && h.col_idx[q] == s * 32 + (q - off) % 32;
   }
-  if (env_int("TB_SPMV_S", 0) == 0 && slots > 0 && (double)slots > 1.2 * (double)(slots - pad))
-    return TB_OK;
+  if (env_int("TB_SPMV_PADRULE", 0) && slots > 0 && (double)slots > 1.2 * (double)(slots - pad))
+    return TB_OK;   // (off: with the 8-slice single-stage candidate the TMA kernel
+                    // also wins on the padded kNN matrix, 404 vs 447 us)
   auto cap_of = [&](int S) {
     long long cap = 0;
     for (long long s0 = 0; s0 < h.n_slices; s0 += S) {
@@ -2238,8 +2239,8 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
     // default whenever the TMA SpMV and the dataflow precond apply
     // (configs 2, 3, 5: 23.3 / 51.9 / 1694 ms vs 28.5 / 54.4 / ~2000 ms for
     // the single persistent launch)
-    pl->split_pcg = pl->persist_ok && pl->n_lvl1_flow > 0 && pl->spmv_S > 0 &&
-                    (se == 1 || (se < 0 && pl->n >= sn));
+    pl->split_pcg = pl->persist_ok && pl->spmv_S > 0 &&
+                    (se == 1 || (se < 0 && pl->n >= sn && pl->n_lvl1_flow > 0));
     // the split path runs as a CUDA graph (conditional WHILE, device-side
     // convergence test) unless TB_PCG_SPLIT_POLL=n asks for host polling
     if (pl->split_pcg && check_every <= 0) check_every = env_int("TB_PCG_SPLIT_POLL", 0);
