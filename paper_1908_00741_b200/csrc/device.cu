@@ -368,7 +368,9 @@ __global__ void __launch_bounds__(kBlock)
   }
 
 // x += alpha p; r -= alpha ap; rel = ||r|| / ||b|| (src/solver.py:178-186).
-template <bool PAIRS = false>
+// FOLDX: x += alpha p is deferred to the next p update (cg_rz_p_coop<true>)
+// or, after the loop, to cg_x_final -- this pass then only streams r and ap.
+template <bool PAIRS = false, bool FOLDX = false>
 __global__ void __launch_bounds__(kBlock)
     cg_update_xr(long long n, const double *__restrict__ p,
                  const double *__restrict__ ap, double *__restrict__ x,
@@ -379,14 +381,17 @@ __global__ void __launch_bounds__(kBlock)
   double part = 0.0;
   if (PAIRS) {   // 16-byte accesses (n even)
     TB_PAIRS4({
-      const double2 xo = *(const double2 *)(x + i), po = *(const double2 *)(p + i);
+      if (!FOLDX) {
+        const double2 xo = *(const double2 *)(x + i), po = *(const double2 *)(p + i);
+        double2 xn;
+        xn.x = __dadd_rn(xo.x, __dmul_rn(alpha, po.x));
+        xn.y = __dadd_rn(xo.y, __dmul_rn(alpha, po.y));
+        *(double2 *)(x + i) = xn;
+      }
       const double2 ro = *(const double2 *)(r + i), ao = *(const double2 *)(ap + i);
-      double2 xn, rn;
-      xn.x = __dadd_rn(xo.x, __dmul_rn(alpha, po.x));
-      xn.y = __dadd_rn(xo.y, __dmul_rn(alpha, po.y));
+      double2 rn;
       rn.x = __dsub_rn(ro.x, __dmul_rn(alpha, ao.x));
       rn.y = __dsub_rn(ro.y, __dmul_rn(alpha, ao.y));
-      *(double2 *)(x + i) = xn;
       *(double2 *)(r + i) = rn;
       part += rn.x * rn.x;
       part += rn.y * rn.y;
@@ -520,12 +525,15 @@ __global__ void __launch_bounds__(spmv_tma::kThreads, 2)
 // cg_rz's last-CTA reduction, and the p update follows without a second
 // launch.  Every CTA reads the old rz before the barrier; CTA 0 publishes
 // the new rz / beta after it.
+template <bool FOLDX = false>
 __global__ void __launch_bounds__(kBlock)
     cg_rz_p_coop(long long n, const double *__restrict__ r, const double *__restrict__ z,
-                 double *__restrict__ p, double *partials, unsigned *bar, PcgState *st) {
+                 double *__restrict__ p, double *partials, unsigned *bar, PcgState *st,
+                 double *__restrict__ x) {
   __shared__ double sh[33];
   if (st->done) return;
   const double rz_old = st->rz;
+  const double alpha = st->alpha;   // this iteration's, for the deferred x update
   double part = 0.0;
   TB_PAIRS4({
     const double2 zi = *(const double2 *)(z + i), ri = *(const double2 *)(r + i);
@@ -536,6 +544,13 @@ __global__ void __launch_bounds__(kBlock)
   const double beta = rzn / rz_old;
   TB_PAIRS4({
     const double2 zi = *(const double2 *)(z + i), po = *(const double2 *)(p + i);
+    if (FOLDX) {   // x += alpha p with the p this iteration's x/r pass used
+      const double2 xo = *(const double2 *)(x + i);
+      double2 xn;
+      xn.x = __dadd_rn(xo.x, __dmul_rn(alpha, po.x));
+      xn.y = __dadd_rn(xo.y, __dmul_rn(alpha, po.y));
+      *(double2 *)(x + i) = xn;
+    }
     double2 pn;
     pn.x = __dadd_rn(zi.x, __dmul_rn(beta, po.x));
     pn.y = __dadd_rn(zi.y, __dmul_rn(beta, po.y));
@@ -545,6 +560,18 @@ __global__ void __launch_bounds__(kBlock)
     st->beta = beta;
     st->rz = rzn;
   }
+}
+
+// After the loop of a FOLDX solve: the last iteration's x += alpha p (its
+// p update never ran: every exit happens at the residual check or before).
+__global__ void __launch_bounds__(kBlock)
+    cg_x_final(long long n, const double *__restrict__ p, double *__restrict__ x,
+               const PcgState *st) {
+  if (st->status != TB_OK || st->iter < 1) return;
+  const double alpha = st->alpha;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
 }
 
 // rz_new = r . z; beta = rz_new / rz; rz = rz_new (src/solver.py:190-192).
@@ -1405,6 +1432,22 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
 int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, const double *b,
                       double *x, cudaStream_t s, long long applications);
 
+// x += alpha p folded into the p update (TB_FOLD_X=0 disables): only with
+// the cooperative r.z + p kernel, which then owns that update.
+bool fold_x(const tb_plan *pl) {
+  return (pl->n % 2) == 0 && env_int("TB_VEC_PAIRS", 1) && pl->rzp_grid > 0 && pl->bar &&
+         env_int("TB_FOLD_X", 1);
+}
+
+// The deferred x update of the last iteration (FOLDX solves).
+int launch_x_final(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
+  if (!fold_x(pl)) return TB_OK;
+  cg_x_final<<<reduce_grid(pl->n, pl->vec_pt), kBlock, 0, s>>>(pl->n, pl->p, x, pl->st);
+  ++*nl;
+  CU(cudaGetLastError());
+  return TB_OK;
+}
+
 // z = M r inside a kernel-sequence iteration: the per-color phase kernels,
 // or (split mode, host-polled loop only: the launch takes a fresh epoch from
 // the host) one persistent dataflow launch.
@@ -1450,8 +1493,9 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
     if ((rc = launch_spmv(pl, pl->p, pl->ap, s, true, nl))) return rc;
     if ((rc = debug_sync(pl, s, "spmv+dot"))) return rc;
     const bool pairs = (n % 2) == 0 && env_int("TB_VEC_PAIRS", 1);
-    (pairs ? cg_update_xr<true> : cg_update_xr<false>)<<<rg, kBlock, 0, s>>>(
-        n, pl->p, pl->ap, x, pl->r, pl->partials, pl->st, pl->hist);
+    const bool fold = fold_x(pl);
+    (fold ? cg_update_xr<true, true> : pairs ? cg_update_xr<true> : cg_update_xr<false>)
+        <<<rg, kBlock, 0, s>>>(n, pl->p, pl->ap, x, pl->r, pl->partials, pl->st, pl->hist);
     ++*nl;
     if ((rc = debug_sync(pl, s, "cg_update_xr"))) return rc;
   }
@@ -1461,12 +1505,13 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   if (pairs2 && pl->rzp_grid > 0 && pl->bar) {
     long long nn = n;
     const double *rr = pl->r, *zz = pl->z;
-    double *pp = pl->p, *pa = pl->partials;
+    double *pp = pl->p, *pa = pl->partials, *xx = x;
     unsigned *bb = pl->bar;
     PcgState *ss = pl->st;
-    void *args[] = {&nn, &rr, &zz, &pp, &pa, &bb, &ss};
-    CU(cudaLaunchCooperativeKernel((const void *)cg_rz_p_coop, dim3(pl->rzp_grid),
-                                   dim3(kBlock), args, 0, s));
+    void *args[] = {&nn, &rr, &zz, &pp, &pa, &bb, &ss, &xx};
+    CU(cudaLaunchCooperativeKernel(fold_x(pl) ? (const void *)cg_rz_p_coop<true>
+                                              : (const void *)cg_rz_p_coop<false>,
+                                   dim3(pl->rzp_grid), dim3(kBlock), args, 0, s));
     --*nl;   // one launch instead of two
   } else {
     (pairs2 ? cg_rz<false, true> : cg_rz<false, false>)<<<rg, kBlock, 0, s>>>(
@@ -1560,6 +1605,16 @@ int build_graph(tb_plan *pl, const double *b, double *x) {
   if (rc) return rc;
   CU(ce);
   pl->launches_per_iter = nl;
+  if (fold_x(pl)) {   // epilogue after the loop: the last iteration's x update
+    long long ne = 0;
+    CU(cudaStreamBeginCaptureToGraph(pl->stream, g, &cnode, nullptr, 1,
+                                     cudaStreamCaptureModeThreadLocal));
+    rc = launch_x_final(pl, x, pl->stream, &ne);
+    ce = cudaStreamEndCapture(pl->stream, &captured);
+    if (rc) return rc;
+    CU(ce);
+    pl->launches_prologue += ne;
+  }
   CU(cudaGraphInstantiate(&pl->gexec, g, 0));
   pl->g_b = b;
   pl->g_x = x;
@@ -1712,7 +1767,7 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
   if (env_int("TB_RZP_FUSE", 1)) {   // fused r.z + p update for the kernel-sequence paths
     int ps = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cg_rz_p_coop, kBlock, 0));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cg_rz_p_coop<true>, kBlock, 0));
     const long long want = ((pl->n + 1) / 2 + kBlock * 8 - 1) / (kBlock * 8);  // ~16 elements/thread
     long long g = (long long)ps * pl->num_sms;
     if (want < g) g = want;
@@ -2277,6 +2332,7 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
       ++polls;
       if (hs.done) break;
     }
+    if ((rc = launch_x_final(pl, x, pl->stream, &polled_launches))) return rc;
     // restore the graph-loop fields for the next graph run
     PcgState tmp = hs;
     tmp.loop = h;
