@@ -529,7 +529,7 @@ template <bool FOLDX = false>
 __global__ void __launch_bounds__(kBlock)
     cg_rz_p_coop(long long n, const double *__restrict__ r, const double *__restrict__ z,
                  double *__restrict__ p, double *partials, unsigned *bar, PcgState *st,
-                 double *__restrict__ x) {
+                 double *__restrict__ x, unsigned *epoch_bump) {
   __shared__ double sh[33];
   if (st->done) return;
   const double rz_old = st->rz;
@@ -559,6 +559,7 @@ __global__ void __launch_bounds__(kBlock)
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->beta = beta;
     st->rz = rzn;
+    if (epoch_bump) *epoch_bump += 1u;   // graph-replayed precond: next epoch
   }
 }
 
@@ -1019,6 +1020,7 @@ struct tb_plan {
   int xr_grid = 0;             // spmv_tma_xr cooperative grid (0 = separate x/r pass)
   int rzp_grid = 0;            // cg_rz_p_coop cooperative grid (0 = cg_rz + cg_update_p)
   bool in_graph = false;       // capturing the split graph: precond epochs from epoch_dev
+  bool defer_bump = false;     // the iteration's cg_rz_p_coop bumps the epoch instead
   bool g_split = false;        // the instantiated graph is the split variant
   unsigned *epoch_dev = nullptr;
 };
@@ -1455,7 +1457,7 @@ int launch_precond_step(tb_plan *pl, cudaStream_t s, long long *nl) {
   int rc;
   if (pl->split_pcg) {
     if ((rc = launch_persistent(pl, 0, pl->r, pl->z, nullptr, nullptr, s, 1))) return rc;
-    *nl += pl->in_graph ? 2 : 1;   // + the epoch bump
+    *nl += (pl->in_graph && !pl->defer_bump) ? 2 : 1;   // + the epoch bump
     return TB_OK;
   }
   if ((rc = launch_forward(pl, pl->r, pl->y, s, pl->st, nl))) return rc;
@@ -1499,7 +1501,13 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
     ++*nl;
     if ((rc = debug_sync(pl, s, "cg_update_xr"))) return rc;
   }
-  if ((rc = launch_precond_step(pl, s, nl))) return rc;
+  const bool coop_p = (n % 2) == 0 && env_int("TB_VEC_PAIRS", 1) && pl->rzp_grid > 0 && pl->bar;
+  pl->defer_bump = pl->in_graph && pl->split_pcg && pl->n_lvl1_flow > 0 && coop_p;
+  rc = launch_precond_step(pl, s, nl);
+  if (rc) {
+    pl->defer_bump = false;
+    return rc;
+  }
   if ((rc = debug_sync(pl, s, "precond"))) return rc;
   const bool pairs2 = (n % 2) == 0 && env_int("TB_VEC_PAIRS", 1);
   if (pairs2 && pl->rzp_grid > 0 && pl->bar) {
@@ -1508,7 +1516,9 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
     double *pp = pl->p, *pa = pl->partials, *xx = x;
     unsigned *bb = pl->bar;
     PcgState *ss = pl->st;
-    void *args[] = {&nn, &rr, &zz, &pp, &pa, &bb, &ss, &xx};
+    unsigned *eb = pl->defer_bump ? pl->epoch_dev : nullptr;
+    pl->defer_bump = false;
+    void *args[] = {&nn, &rr, &zz, &pp, &pa, &bb, &ss, &xx, &eb};
     CU(cudaLaunchCooperativeKernel(fold_x(pl) ? (const void *)cg_rz_p_coop<true>
                                               : (const void *)cg_rz_p_coop<false>,
                                    dim3(pl->rzp_grid), dim3(kBlock), args, 0, s));
@@ -1871,7 +1881,7 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
     } else {
       pcg_persistent_fn_launch(pl, P, s);
     }
-    epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
+    if (!pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
     CU(cudaGetLastError());
     return TB_OK;
   }
@@ -2364,6 +2374,9 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
       CU(cudaMemcpyAsync(&pl->epoch, pl->epoch_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
                          pl->stream));
     CU(cudaStreamSynchronize(pl->stream));
+    // the last application may not have bumped (the loop stopped before its
+    // p update): never reuse its epoch
+    if (pl->split_pcg) ++pl->epoch;
   }
   pl->split_pcg = false;
   if ((rc = sync_out(pl, stream))) return rc;
