@@ -333,7 +333,7 @@ def run_ours(args, rank, world, local_rank):
     sp_ms = tsp.times_ms()[args.warmup:]
     sp_us = 1e3 * sum(sp_ms) / len(sp_ms)
     sp_bytes = spmv_bytes(int(a.nnz), a.n)
-    spmv_line = {"kernel": "spmv_sell (thread per row, 8 slots in flight)",
+    spmv_line = {"kernel": "plan SpMV: spmv_tma (TMA-staged SELL chunks); thread per row if no TMA candidate fits",
                  "algorithmic_bytes": sp_bytes, "avg_us": sp_us,
                  "achieved": sp_bytes / (sp_us / 1e6) / 1e9, "peak": peak, "unit": "GB/s",
                  "frac": sp_bytes / (sp_us / 1e6) / 1e9 / peak}
