@@ -342,10 +342,10 @@ def run_ours(args, rank, world, local_rank):
     # Every step copies its rhs from pinned host memory, applies the
     # preconditioner and copies z back to pinned host memory.  Steps are
     # software-pipelined over three streams with double-buffered device
-    # vectors (H2D of step i+1 and D2H of step i-1 overlap step i's sweeps;
+    # vectors (three buffers; H2D of step i+1 and D2H of step i-1 overlap step i's sweeps;
     # PCIe is full duplex), as a caller streaming right-hand sides would run
     # it.  Timed from the first H2D to the last D2H on the device.
-    nbuf = int(os.environ.get("TB_E2E_NBUF", "2"))
+    nbuf = int(os.environ.get("TB_E2E_NBUF", "3"))
     r_host = torch.from_numpy(np.random.default_rng(0).standard_normal(n_pad)).pin_memory()
     z_host = [torch.empty(n_pad, dtype=torch.float64).pin_memory() for _ in range(nbuf)]
     r_dev = [torch.empty(n_pad, dtype=torch.float64, device=dev) for _ in range(nbuf)]
@@ -385,6 +385,25 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     e2e_ms = e2e_run(args.steps)
     barrier()
+
+    # The host-link floor of that pipeline: the same H2D and D2H copies issued
+    # concurrently with no compute (PCIe is full duplex), per step.
+    def link_run(k):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(s_in)
+        s_out.wait_stream(s_in)
+        for i in range(k):
+            with torch.cuda.stream(s_in):
+                r_dev[i % nbuf].copy_(r_host, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                z_host[i % nbuf].copy_(z_dev[i % nbuf], non_blocking=True)
+        s_in.wait_stream(s_out)
+        t1.record(s_in)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / k
+
+    link_run(2)
+    link_ms = link_run(max(args.steps, 10))
 
     # ---------------- ICCG time-to-solution on the device
     b_dev = torch.from_numpy(setup.b_sys).to(dev)
@@ -455,7 +474,9 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_val, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * n_pad, "d2h_bytes_per_step": 8 * n_pad,
                     "ms_per_step": e2e_ms_max / args.steps,
-                    "pipeline": f"H2D / precond / D2H on 3 streams, {nbuf} device buffers"},
+                    "pipeline": f"H2D / precond / D2H on 3 streams, {nbuf} device buffers",
+                    "link_floor_ms_per_step": link_ms,
+                    "frac_of_link_floor": link_ms / (e2e_ms_max / args.steps)},
             "gpu_launches": args.steps if pinfo["precond"] else launches,
             "clocks": clk.summary(),
             "iccg": {"iterations": int(rep.iterations),
