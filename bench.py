@@ -341,10 +341,10 @@ def run_ours(args, rank, world, local_rank):
     # ---------------- e2e through the public API (host buffers)
     # Every step copies its rhs from pinned host memory, applies the
     # preconditioner and copies z back to pinned host memory.  Steps are
-    # software-pipelined over three streams with double-buffered device
-    # vectors (three buffers; H2D of step i+1 and D2H of step i-1 overlap step i's sweeps;
-    # PCIe is full duplex), as a caller streaming right-hand sides would run
-    # it.  Timed from the first H2D to the last D2H on the device.
+    # software-pipelined over three streams with TB_E2E_NBUF (3) rotating
+    # device vectors (H2D of step i+1 and D2H of step i-1 overlap step i's
+    # sweeps; PCIe is full duplex), as a caller streaming right-hand sides
+    # would run it.  Timed from the first H2D to the last D2H on the device.
     nbuf = int(os.environ.get("TB_E2E_NBUF", "3"))
     r_host = torch.from_numpy(np.random.default_rng(0).standard_normal(n_pad)).pin_memory()
     z_host = [torch.empty(n_pad, dtype=torch.float64).pin_memory() for _ in range(nbuf)]
