@@ -20,8 +20,11 @@ value    = algorithmic bytes of the two sweeps (2 * (12 nnz_L + 32 N), SURVEY
            8(d)) x steps x ranks / max-over-ranks summed device time.
 e2e      = the same through the public API with host buffers: pinned host r
            -> device, fwd+bwd, z -> pinned host, copies inside the timed region.
-roofline = the sweep kernel (one launch per color phase): algorithmic bytes
-           of the launch / its CUDA-event duration, vs MEASURED_PEAKS.json.
+roofline = the precond kernel (N = 1: the persistent dataflow kernel, both
+           sweeps in one launch, when the plan has one; else the per-color
+           sweep launches): algorithmic bytes per launch / its CUDA-event
+           duration, vs MEASURED_PEAKS.json.  `spmv` is the same for the
+           plan SpMV.  e2e also reports the host-link floor.
 iccg     = full PCG solve to 1e-7 on the device (one CUDA-graph launch).
 cpu_baseline = the CPU oracle port of the reference path (oracle/), all host
            threads, bounded sample of the same sweep workload (rank 0, N=1).
