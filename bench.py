@@ -315,6 +315,7 @@ def run_ours(args, rank, world, local_rank):
         n_launch = len(lt)
     achieved = tot_b / (tot_ms / 1e3) / 1e9
     traffic, traffic_src = args.traffic, "--traffic" if args.traffic else None
+    tj = {}
     if traffic is None:
         tp = os.path.join(HERE, "profiles", "traffic.json")
         if os.path.exists(tp):
@@ -339,7 +340,9 @@ def run_ours(args, rank, world, local_rank):
     spmv_line = {"kernel": "plan SpMV: spmv_tma (TMA-staged SELL chunks); thread per row if no TMA candidate fits",
                  "algorithmic_bytes": sp_bytes, "avg_us": sp_us,
                  "achieved": sp_bytes / (sp_us / 1e6) / 1e9, "peak": peak, "unit": "GB/s",
-                 "frac": sp_bytes / (sp_us / 1e6) / 1e9 / peak}
+                 "frac": sp_bytes / (sp_us / 1e6) / 1e9 / peak,
+                 "traffic": tj.get("spmv_tma", {}).get("dram_bytes_per_launch") if not args.traffic else None,
+                 "traffic_source": tj.get("spmv_tma", {}).get("source") if not args.traffic else None}
 
     # ---------------- e2e through the public API (host buffers)
     # Every step copies its rhs from pinned host memory, applies the
