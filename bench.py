@@ -2,13 +2,15 @@
 """Benchmark: HBMC IC(0) fwd+bwd substitution GB/s and ICCG time-to-solution.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 2]
+                    [--config 5]
 
-Workload (BASELINE.json configs[1]): 3-D variable-coefficient 7-point
-diffusion on 128^3, HBMC b_s=8, w=32, fp64, synthetic seeded inputs
-(SURVEY.md Appendix B).  One "step" = one preconditioner application
-z = (L L^T)^-1 r on the device (forward + backward HBMC sweep, all color
-phases), inputs resident in HBM.
+Workload (default): BASELINE.json configs[4], the largest configuration that
+fits one B200 -- anisotropic 3-D 7-point on 512^3 (N = 134,217,728,
+nnz = 937,951,232), HBMC b_s=16, w=32, fp64, synthetic seeded inputs
+(SURVEY.md Appendix B).  `--config 2` (configs[1], 128^3 variable
+coefficient, b_s=8) and the others remain selectable.  One "step" = one
+preconditioner application z = (L L^T)^-1 r on the device (forward +
+backward HBMC sweep, all color phases), inputs resident in HBM.
 
 Timing: CUDA events on the launching stream, created up front; every timed
 step is enqueued without a host synchronisation (so host launch overhead
@@ -18,16 +20,29 @@ write-back lands in the timed kernel).
 
 value    = algorithmic bytes of the two sweeps (2 * (12 nnz_L + 32 N), SURVEY
            8(d)) x steps x ranks / max-over-ranks summed device time.
-e2e      = the same through the public API with host buffers: pinned host r
-           -> device, fwd+bwd, z -> pinned host, copies inside the timed region.
+e2e      = the same through the C-ABI plan operator with HOST buffers: pinned
+           host r -> device, fwd+bwd, z -> pinned host, copies inside the
+           timed region (pipelined over 3 streams, as a caller streaming
+           right-hand sides runs it).  e2e.api = per-call timings of the
+           trilab-facing calls a user makes: apply_ic_preconditioner(numpy r)
+           (pageable, synchronous) and the ICCG solve b (host) -> x (host).
 roofline = the precond kernel (N = 1: the persistent dataflow kernel, both
            sweeps in one launch, when the plan has one; else the per-color
            sweep launches): algorithmic bytes per launch / its CUDA-event
            duration, vs MEASURED_PEAKS.json.  `spmv` is the same for the
-           plan SpMV.  e2e also reports the host-link floor.
+           plan SpMV.  traffic = ncu dram bytes of that kernel
+           (profiles/traffic.json).
 iccg     = full PCG solve to 1e-7 on the device (one CUDA-graph launch).
-cpu_baseline = the CPU oracle port of the reference path (oracle/), all host
-           threads, bounded sample of the same sweep workload (rank 0, N=1).
+cpu_baseline = the CPU oracle port of the reference path (oracle/): the
+           reference's fwd_sell_range / bwd_sell_range restated in C, timed
+           on this product's SELL arrays (SURVEY 8(d) for config 5), all
+           host threads and 1 thread, bounded samples (rank 0, N=1).
+
+--impl reference: the reference's CPU path on this box's host cores -- the
+oracle port (oracle/), which imports nothing from the product: matrix
+assembled with the oracle's coo_to_csr, the oracle's own ordering / IC(0) /
+SELL build, steps = full fwd+bwd HBMC sweeps with all threads, plus a
+bounded ICCG sample (src/solver.py:139-204 with all threads).
 
 N > 1 (torchrun, one rank per GPU, NCCL): the row-partitioned solve of
 SURVEY 8(e) -- every color's level-1 blocks split over the ranks, one halo
@@ -132,55 +147,155 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def build_problem(cfg_id):
-    from paper_1908_00741_b200 import problems
-    label, gen, bs, w = problems.CONFIGS[cfg_id]
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def build_problem(cfg_id, backend="product"):
+    import workloads
     t0 = time.perf_counter()
-    a = gen()
-    xs, b = problems.rhs(a)
+    label, a, bs, w = workloads.generate(cfg_id, backend=backend)
+    xs, b = workloads.rhs(a, backend=backend)
     return label, a, xs, b, bs, w, time.perf_counter() - t0
 
 
-def cpu_baseline(a, b, bs, w, steps, warmup, threads):
-    """Oracle port of the reference CPU path: fwd+bwd HBMC sweep, GB/s."""
-    from oracle import oracle as O
-    oa = O.Csr(a.n, a.row_ptr, a.col_idx, a.vals)
-    osys = O.HbmcSystem(oa, b, bs, w)
-    r = np.random.default_rng(0).standard_normal(osys.hl["n_pad"])
-    for _ in range(warmup):
-        osys.precond(r, threads)
+def load_digest(cfg_id):
+    p = os.path.join(HERE, "tests", "golden", f"config{cfg_id}_digest.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as fh:
+        return json.load(fh)
+
+
+def time_sweeps(O, Ls, Us, inv_d, hl, r, threads, reps):
+    """Seconds per fwd+bwd HBMC sweep pair (oracle kernels, fork-join per
+    color over `threads` as src/precond.py:377-392)."""
     ts = []
-    for _ in range(steps):
+    for _ in range(reps):
         t0 = time.perf_counter()
-        osys.precond(r, threads)
+        y = O.hbmc_sweep(True, Ls, inv_d, r, hl, threads)
+        O.hbmc_sweep(False, Us, inv_d, y, hl, threads)
         ts.append(time.perf_counter() - t0)
-    nbytes = 2 * sweep_bytes(osys.nnz_L, a.n)
-    return {"value": nbytes * len(ts) / sum(ts) / 1e9, "unit": "GB/s",
-            "cores": threads, "kind": "port",
-            "sample": f"{len(ts)} fwd+bwd HBMC sweeps of the full workload "
-                      f"(oracle/hbmc_oracle.c, per-color fork-join over {threads} "
-                      f"OpenMP threads as src/precond.py:377-392)",
-            "ms_per_step": 1e3 * sum(ts) / len(ts),
-            "setup_s": osys.time_setup_s}, osys
+    return ts
+
+
+def cpu_baseline_on_arrays(Ls, Us, inv_d, hl, nbytes, threads, reps_all, t1_budget_s=30.0):
+    """The reference's sweep kernels (oracle port) on the given SELL arrays:
+    all threads (`reps_all` applications, after one warm-up) and 1 thread
+    (one application, or a bounded share of the level-1 blocks of every
+    color when a whole one would exceed `t1_budget_s`)."""
+    from oracle import oracle as O
+    r = np.random.default_rng(0).standard_normal(hl["n_pad"])
+    time_sweeps(O, Ls, Us, inv_d, hl, r, threads, 1)
+    ts = time_sweeps(O, Ls, Us, inv_d, hl, r, threads, reps_all)
+    t_all = sum(ts) / len(ts)
+    # 1 thread: estimate from the all-thread time x threads, then sample a
+    # fraction of every color's level-1 range sized to the budget
+    frac = min(1.0, t1_budget_s / max(1e-9, t_all * threads))
+    if frac >= 1.0:
+        t1 = time_sweeps(O, Ls, Us, inv_d, hl, r, 1, 1)[0]
+        t1_desc = "one full fwd+bwd application"
+    else:
+        # the first ceil(frac * nbar(c)) level-1 blocks of every color, fwd
+        # then bwd (same kernels, same per-block work), scaled pro rata
+        cl = np.asarray(hl["color_lvl1_ranges"], dtype=np.int64)
+        keep = np.maximum(1, np.ceil(frac * np.diff(cl)).astype(np.int64))
+        y = np.zeros(hl["n_pad"])
+        z = np.zeros(hl["n_pad"])
+        t0 = time.perf_counter()
+        for c in range(hl["n_c"]):
+            O.LIB.or_fwd_sell_range(Ls.slice_ptr, Ls.slice_len, Ls.col_idx, Ls.vals, inv_d,
+                                    r, y, hl["w"], hl["b_s"], int(cl[c]), int(cl[c] + keep[c]))
+        for c in range(hl["n_c"] - 1, -1, -1):
+            O.LIB.or_bwd_sell_range(Us.slice_ptr, Us.slice_len, Us.col_idx, Us.vals, inv_d,
+                                    y, z, hl["w"], hl["b_s"], int(cl[c]), int(cl[c] + keep[c]))
+        frac_done = float(keep.sum()) / float(cl[-1])
+        t1 = (time.perf_counter() - t0) / frac_done
+        t1_desc = (f"the first {100 * frac_done:.2f} % of every color's level-1 blocks "
+                   f"(fwd then bwd), scaled to the whole application")
+    return {"value": nbytes / t_all / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+            "cpu": cpu_model(),
+            "sample": f"{reps_all} fwd+bwd HBMC applications of the full workload after "
+                      f"1 warm-up (oracle/hbmc_oracle.c fwd/bwd_sell_range, per-color "
+                      f"fork-join over {threads} OpenMP threads as src/precond.py:377-392)",
+            "ms_per_step": 1e3 * t_all,
+            "t1": {"value": nbytes / t1 / 1e9, "unit": "GB/s", "cores": 1,
+                   "ms_per_step": 1e3 * t1, "sample": t1_desc}}
 
 
 def run_reference(args, rank):
+    """The reference's CPU path, import-clean: nothing from the product
+    package is imported (the matrix is assembled by the oracle's C
+    coo_to_csr), so only oracle/liboracle.so is loaded."""
     if rank != 0:
         return
     from oracle import oracle as O
-    label, a, xs, b, bs, w, _ = build_problem(args.config)
     threads = O.max_threads()
-    cb, osys = cpu_baseline(a, b, bs, w, args.steps, args.warmup, threads)
-    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s",
+    label, a, xs, b, bs, w, t_gen = build_problem(args.config, backend="oracle")
+    n, nnz_a = a.n, int(a.nnz)
+    osys = O.HbmcSystem(a, b, bs, w, lean=True)
+    del a
+    hl = osys.hl
+    nbytes = 2 * sweep_bytes(osys.nnz_L, n)
+    r = np.random.default_rng(0).standard_normal(hl["n_pad"])
+    time_sweeps(O, osys.Ls, osys.Us, osys.inv_d, hl, r, threads, args.warmup)
+    ts = time_sweeps(O, osys.Ls, osys.Us, osys.inv_d, hl, r, threads, args.steps)
+    value = nbytes * len(ts) / sum(ts) / 1e9
+    cb = cpu_baseline_on_arrays(osys.Ls, osys.Us, osys.inv_d, hl, nbytes, threads, 1)
+    cb["value"] = value
+    cb["ms_per_step"] = 1e3 * sum(ts) / len(ts)
+    cb["sample"] = (f"{args.steps} timed fwd+bwd HBMC applications of the full workload "
+                    f"after {args.warmup} warm-ups (oracle/hbmc_oracle.c fwd/bwd_sell_range, "
+                    f"per-color fork-join over {threads} OpenMP threads as "
+                    f"src/precond.py:377-392), oracle-built system")
+    cb["setup_s"] = osys.time_setup_s
+    # ICCG (src/solver.py:139-204, all threads incl. the SELL SpMV): the
+    # whole solve when it is short, else a bounded number of iterations
+    dg = load_digest(args.config)
+    ref_iters = (dg.get("hbmc") or {}).get("iterations")
+    t0 = time.perf_counter()
+    _, it1, _, _ = O.pcg_hbmc(osys, max_iters=1, threads=threads, spmv_threads=threads)
+    t_first = time.perf_counter() - t0
+    est_total = t_first * (ref_iters or 1)
+    if est_total <= args.ref_iccg_budget_s:
+        t0 = time.perf_counter()
+        _, it, _, conv = O.pcg_hbmc(osys, threads=threads, spmv_threads=threads)
+        iccg = {"iterations": it, "converged": conv,
+                "time_to_solution_s": time.perf_counter() - t0, "kind": "full solve"}
+    else:
+        k = max(2, int(args.ref_iccg_budget_s / max(t_first, 1e-9)))
+        t0 = time.perf_counter()
+        _, it, _, conv = O.pcg_hbmc(osys, max_iters=k, threads=threads, spmv_threads=threads)
+        dt = time.perf_counter() - t0
+        per_it = dt / max(1, it)
+        iccg = {"sampled_iterations": it, "s_per_iteration": per_it,
+                "iterations_to_1e-7": ref_iters,
+                "time_to_solution_s_estimated": per_it * ref_iters if ref_iters else None,
+                "kind": f"first {it} iterations timed, x the oracle's iteration count "
+                        f"(tests/golden/config{args.config}_digest.json)",
+                "full_solve_s_offline": (dg.get("hbmc") or {}).get("time_solve_s"),
+                "full_solve_offline_source": dg.get("source")}
+    iccg["threads"] = threads
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+            "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, SURVEY Appendix B)",
             "config": {"workload": f"config{args.config} {label} b_s={bs} w={w}",
-                       "N": a.n, "nnz_L": osys.nnz_L},
+                       "N": n, "n_pad": int(hl["n_pad"]), "nnz_A": nnz_a,
+                       "nnz_L": int(osys.nnz_L), "n_c": int(hl["n_c"]),
+                       "bytes_per_step": nbytes},
             "cpu_baseline": cb,
-            "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "iccg": iccg, "generate_s": t_gen}
     print(json.dumps(line), flush=True)
 
 
@@ -216,17 +331,19 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     label, a, xs, b, bs, w, t_gen = build_problem(args.config)
+    n, nnz_a = a.n, int(a.nnz)
     cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
     t0 = time.perf_counter()
     setup = solver.prepare(a, b, cfg)
     t_host = time.perf_counter() - t0
+    del a
     solver.attach_plan(setup, cfg)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     plan, hl = setup.plan, setup.layout
     n_pad = hl.n_pad
-    nnz_l = int((a.nnz - a.n) // 2)   # strictly-lower nonzeros of A (= of L)
-    step_bytes = 2 * sweep_bytes(nnz_l, a.n)
+    nnz_l = (nnz_a - n) // 2   # strictly-lower nonzeros of A (= of L)
+    step_bytes = 2 * sweep_bytes(nnz_l, n)
 
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
@@ -264,8 +381,8 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- per-launch timing of the sweep kernel (roofline)
     span = bs * w
-    lower_counts = np.diff(P.precond._strict_tri(setup.a_sys).row_ptr)
-    upper_counts = np.diff(P.precond._strict_tri(setup.a_sys, upper=True).row_ptr)
+    lower_counts = P.precond.tri_row_counts(setup.a_sys)
+    upper_counts = P.precond.tri_row_counts(setup.a_sys, upper=True)
     real = np.zeros(n_pad, dtype=bool)
     real[hl.real_positions] = True
     phases = []
@@ -291,8 +408,7 @@ def run_ours(args, rank, world, local_rank):
         ts = lt[q::len(phases)]
         info = plan.phase_info(fw, c)
         per_phase.append({"sweep": "fwd" if fw else "bwd", "color": c,
-                          "kernel": {0: "simple", 1: "staged", 2: "ring", 3: "reg",
-                                     4: "lean", 5: "cta", 6: "async"}[info["staged"]],
+                          "kernel": "lean" if info["staged"] == 4 else "simple",
                           "bytes": nb, "avg_us": 1e3 * sum(ts) / len(ts),
                           "GBps": nb / (sum(ts) / len(ts) / 1e3) / 1e9})
     peak, peak_src = load_peaks()
@@ -336,7 +452,7 @@ def run_ours(args, rank, world, local_rank):
         tsp.stop()
     sp_ms = tsp.times_ms()[args.warmup:]
     sp_us = 1e3 * sum(sp_ms) / len(sp_ms)
-    sp_bytes = spmv_bytes(int(a.nnz), a.n)
+    sp_bytes = spmv_bytes(nnz_a, n)
     spmv_line = {"kernel": "plan SpMV: spmv_tma (TMA-staged SELL chunks); thread per row if no TMA candidate fits",
                  "algorithmic_bytes": sp_bytes, "avg_us": sp_us,
                  "achieved": sp_bytes / (sp_us / 1e6) / 1e9, "peak": peak, "unit": "GB/s",
@@ -433,6 +549,19 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         solver.solve_on_device(setup, cfg)
         t_e2e_solve.append(time.perf_counter() - t0)
+    # the trilab-facing preconditioner call a user makes: numpy r in, numpy
+    # z out (pageable host memory, synchronous; src/precond.py:411-425).  The
+    # first call builds and uploads the factor plan (untimed).
+    r_np = np.random.default_rng(0).standard_normal(n_pad)
+    P.apply_ic_preconditioner("hbmc", setup.factor, hl, r_np)
+    t_api = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        P.apply_ic_preconditioner("hbmc", setup.factor, hl, r_np)
+        t_api.append(time.perf_counter() - t0)
+    P.precond.release_plans(setup.factor)
+    del r_np
 
     # ---------------- max over ranks
     def mx(v):
@@ -452,12 +581,14 @@ def run_ours(args, rank, world, local_rank):
         cb = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as O
-            cb, _ = cpu_baseline(a, b, bs, w, min(args.steps, 10), 2, O.max_threads())
-        digest = os.path.join(HERE, "tests", "golden", f"config{args.config}_digest.json")
-        ref = {}
-        if os.path.exists(digest):
-            with open(digest) as fh:
-                ref = json.load(fh).get("hbmc", {})
+            hd = {"n_pad": n_pad, "w": hl.w, "b_s": hl.b_s, "n_c": hl.n_c,
+                  "color_lvl1_ranges": np.asarray(hl.color_lvl1_ranges, dtype=np.int64)}
+            cb = cpu_baseline_on_arrays(setup.factor.lower, setup.factor.upper,
+                                        setup.factor.inv_diag, hd, step_bytes,
+                                        O.max_threads(), 2)
+            cb["sample"] += ", on this product's SELL arrays (SURVEY 8(d))"
+        dg = load_digest(args.config)
+        ref = dg.get("hbmc", {})
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -465,7 +596,7 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, SURVEY Appendix B)",
             "config": {"workload": f"config{args.config} {label} b_s={bs} w={w}",
-                       "N": a.n, "n_pad": n_pad, "nnz_A": int(a.nnz), "nnz_L": nnz_l,
+                       "N": n, "n_pad": n_pad, "nnz_A": nnz_a, "nnz_L": nnz_l,
                        "n_c": hl.n_c, "bytes_per_step": step_bytes,
                        "l2": "flushed before every timed step (256 MiB read)",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
@@ -482,13 +613,19 @@ def run_ours(args, rank, world, local_rank):
                     "ms_per_step": e2e_ms_max / args.steps,
                     "pipeline": f"H2D / precond / D2H on 3 streams, {nbuf} device buffers",
                     "link_floor_ms_per_step": link_ms,
-                    "frac_of_link_floor": link_ms / (e2e_ms_max / args.steps)},
+                    "frac_of_link_floor": link_ms / (e2e_ms_max / args.steps),
+                    "api": {"apply_ic_preconditioner_numpy_ms": 1e3 * min(t_api),
+                            "apply_ic_preconditioner_GBps": step_bytes / min(t_api) / 1e9,
+                            "iccg_host_to_host_ms": 1e3 * min(t_e2e_solve),
+                            "note": "per call, pageable numpy in/out, synchronous"}},
             "gpu_launches": args.steps if pinfo["precond"] else launches,
             "clocks": clk.summary(),
             "iccg": {"iterations": int(rep.iterations),
                      "reference_iterations": ref.get("iterations"),
                      "reference_cpu_solve_s": ref.get("time_solve_s"),
                      "reference_cpu_threads": ref.get("threads"),
+                     "reference_source": dg.get("source", "reference trilab + numba, "
+                                                "survey container (make_golden.py --large)"),
                      "converged": bool(rep.converged),
                      "time_to_solution_ms": min(solves),
                      "ms_per_iteration": min(solves) / max(1, rep.iterations),
@@ -625,7 +762,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--ref-iccg-budget-s", type=float, default=30.0,
+                    help="--impl reference: full ICCG if it fits, else a timed prefix")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="partitioned", choices=["partitioned", "replicas"],
                     help="N > 1: row-partitioned solve (default) or independent replicas")

@@ -272,6 +272,174 @@ void or_color_block_graph(const i64 *row_ptr, const i64 *col_idx, const i64 *blo
     free(mark);
 }
 
+/* ------------------------------------------------------------------ host
+ * Sparse-matrix plumbing of the reference's Python layer restated in C so
+ * the oracle can build the 512^3 config (N = 134M, nnz = 938M) inside the
+ * GPU box's host RAM; each is equivalent to the numpy code it cites. */
+
+/* Row-parallel K:16-23 (same per-row arithmetic, rows independent). */
+void or_spmv_csr_par(i64 n, const i64 *row_ptr, const i64 *col_idx, const double *vals,
+                     const double *x, double *out, int threads) {
+#pragma omp parallel for schedule(static, 4096) num_threads(threads)
+    for (i64 i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (i64 p = row_ptr[i]; p < row_ptr[i + 1]; ++p) s += vals[p] * x[col_idx[p]];
+        out[i] = s;
+    }
+}
+
+typedef struct { i64 c; double v; } cv_t;
+
+static int cv_cmp(const void *a, const void *b) {
+    i64 x = ((const cv_t *)a)->c, y = ((const cv_t *)b)->c;
+    return (x > y) - (x < y);
+}
+
+/* Sort one row's (col, val) pairs by column: insertion sort (stable) for the
+ * short rows of the BASELINE matrices, qsort for long rows.  Returns the
+ * first position whose column equals its predecessor's, or -1. */
+static i64 sort_row(i64 *ci, double *v, i64 len) {
+    if (len <= 64) {
+        for (i64 a = 1; a < len; ++a) {
+            i64 c = ci[a];
+            double x = v[a];
+            i64 b = a - 1;
+            while (b >= 0 && ci[b] > c) { ci[b + 1] = ci[b]; v[b + 1] = v[b]; --b; }
+            ci[b + 1] = c;
+            v[b + 1] = x;
+        }
+    } else {
+        cv_t *t = (cv_t *)malloc(sizeof(cv_t) * (size_t)len);
+        for (i64 a = 0; a < len; ++a) { t[a].c = ci[a]; t[a].v = v[a]; }
+        qsort(t, (size_t)len, sizeof(cv_t), cv_cmp);
+        for (i64 a = 0; a < len; ++a) { ci[a] = t[a].c; v[a] = t[a].v; }
+        free(t);
+    }
+    for (i64 a = 1; a < len; ++a)
+        if (ci[a] == ci[a - 1]) return a;
+    return -1;
+}
+
+/* src/matrix.py:168-197 coo_to_csr (ensure_diagonal=False): entries bucketed
+ * by row, then each row sorted by column == np.lexsort((col, row)); a
+ * duplicate (row, col) is an error.  Returns -1, or the CSR position of the
+ * first duplicate (its row / column are then rp / ci at that position). */
+i64 or_coo_to_csr(i64 n, i64 nnz, const i64 *row, const i64 *col, const double *val,
+                  i64 *rp, i64 *ci, double *v, int threads) {
+    for (i64 i = 0; i <= n; ++i) rp[i] = 0;
+    for (i64 e = 0; e < nnz; ++e) rp[row[e] + 1]++;
+    for (i64 i = 0; i < n; ++i) rp[i + 1] += rp[i];
+    i64 *pos = (i64 *)malloc(sizeof(i64) * (size_t)(n + 1));
+    memcpy(pos, rp, sizeof(i64) * (size_t)(n + 1));
+    for (i64 e = 0; e < nnz; ++e) {
+        i64 p = pos[row[e]]++;
+        ci[p] = col[e];
+        v[p] = val[e];
+    }
+    free(pos);
+    i64 dup = -1;
+#pragma omp parallel for schedule(dynamic, 8192) num_threads(threads)
+    for (i64 i = 0; i < n; ++i) {
+        i64 d = sort_row(ci + rp[i], v + rp[i], rp[i + 1] - rp[i]);
+        if (d >= 0) {
+#pragma omp critical
+            if (dup < 0 || rp[i] + d < dup) dup = rp[i] + d;
+        }
+    }
+    return dup;
+}
+
+/* src/matrix.py:293-304 permute_system's matrix part: entry (i, j) of A
+ * moves to (q[i], q[j]); rows re-sorted by column (the reference's COO ->
+ * lexsort).  Rows are independent. */
+void or_permute_csr(i64 n, const i64 *rp, const i64 *ci, const double *v, const i64 *q,
+                    i64 *rp_out, i64 *ci_out, double *v_out, int threads) {
+    rp_out[0] = 0;
+    for (i64 i = 0; i < n; ++i) rp_out[q[i] + 1] = rp[i + 1] - rp[i];
+    for (i64 i = 0; i < n; ++i) rp_out[i + 1] += rp_out[i];
+#pragma omp parallel for schedule(dynamic, 8192) num_threads(threads)
+    for (i64 i = 0; i < n; ++i) {
+        i64 d = rp_out[q[i]], len = rp[i + 1] - rp[i];
+        for (i64 t = 0; t < len; ++t) {
+            ci_out[d + t] = q[ci[rp[i] + t]];
+            v_out[d + t] = v[rp[i] + t];
+        }
+        sort_row(ci_out + d, v_out + d, len);
+    }
+}
+
+/* src/matrix.py:205-208 csr_transpose: bucket by column, rows visited in
+ * ascending order, so every output row is already column-sorted (== the
+ * lexsort of (row, col) after the swap). */
+void or_csr_transpose(i64 n, const i64 *rp, const i64 *ci, const double *v, i64 *rp_out,
+                      i64 *ci_out, double *v_out) {
+    for (i64 i = 0; i <= n; ++i) rp_out[i] = 0;
+    for (i64 p = 0; p < rp[n]; ++p) rp_out[ci[p] + 1]++;
+    for (i64 i = 0; i < n; ++i) rp_out[i + 1] += rp_out[i];
+    i64 *pos = (i64 *)malloc(sizeof(i64) * (size_t)(n + 1));
+    memcpy(pos, rp_out, sizeof(i64) * (size_t)(n + 1));
+    for (i64 i = 0; i < n; ++i)
+        for (i64 p = rp[i]; p < rp[i + 1]; ++p) {
+            i64 d = pos[ci[p]]++;
+            ci_out[d] = i;
+            v_out[d] = v[p];
+        }
+    free(pos);
+}
+
+/* src/precond.py:163-169 _strict_tri(upper=False) plus A.diagonal()
+ * (src/matrix.py:78-81: 0.0 where a row stores no diagonal).  Pass 1
+ * (lrp == NULL is not allowed): counts into lrp; pass 2 (fill != 0): fill. */
+void or_split_lower(i64 n, const i64 *rp, const i64 *ci, const double *v, i64 *lrp,
+                    i64 *lci, double *lv, double *diag, int fill, int threads) {
+    if (!fill) {
+        lrp[0] = 0;
+#pragma omp parallel for schedule(static, 8192) num_threads(threads)
+        for (i64 i = 0; i < n; ++i) {
+            i64 c = 0;
+            double dg = 0.0;
+            for (i64 p = rp[i]; p < rp[i + 1]; ++p) {
+                if (ci[p] < i) ++c;
+                else if (ci[p] == i) dg = v[p];
+            }
+            lrp[i + 1] = c;
+            diag[i] = dg;
+        }
+        for (i64 i = 0; i < n; ++i) lrp[i + 1] += lrp[i];
+        return;
+    }
+#pragma omp parallel for schedule(static, 8192) num_threads(threads)
+    for (i64 i = 0; i < n; ++i) {
+        i64 d = lrp[i];
+        for (i64 p = rp[i]; p < rp[i + 1]; ++p)
+            if (ci[p] < i) { lci[d] = ci[p]; lv[d] = v[p]; ++d; }
+    }
+}
+
+/* src/matrix.py:211-261 csr_to_sell fill (slice_ptr / slice_len computed by
+ * the caller): padding slots hold column = own row and value 0.0; entry t
+ * of row i at slice_ptr[i / w] + i % w + w * t. */
+void or_csr_to_sell_fill(i64 n, i64 n_slices, i64 w, const i64 *rp, const i64 *ci,
+                         const double *v, const i64 *slice_ptr, const i64 *slice_len,
+                         i64 *col_out, double *val_out, int threads) {
+#pragma omp parallel for schedule(static, 1024) num_threads(threads)
+    for (i64 s = 0; s < n_slices; ++s) {
+        for (i64 t = 0; t < slice_len[s]; ++t)
+            for (i64 j = 0; j < w; ++j) {
+                col_out[slice_ptr[s] + t * w + j] = s * w + j;
+                val_out[slice_ptr[s] + t * w + j] = 0.0;
+            }
+        for (i64 j = 0; j < w; ++j) {
+            i64 i = s * w + j;
+            if (i >= n) break;
+            for (i64 p = rp[i]; p < rp[i + 1]; ++p) {
+                col_out[slice_ptr[s] + j + w * (p - rp[i])] = ci[p];
+                val_out[slice_ptr[s] + j + w * (p - rp[i])] = v[p];
+            }
+        }
+    }
+}
+
 int or_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -19,9 +19,7 @@ OBJDIR = os.path.join(CSRC, "build")
 # (source, extra defines, object name)
 SOURCES = [("builder.cpp", [], "builder"), ("device.cu", [], "device"),
            ("dist.cu", [], "dist"), ("ic0.cu", [], "ic0"),
-           ("mm_parse.cpp", [], "mm_parse")] + [
-    ("sweep_reg_inst.cu", [f"-DTB_FWD={f}", f"-DTB_BS={b}"], f"sweep_reg_{f}_{b}")
-    for f in (1, 0) for b in (16, 8, 4)]
+           ("mm_parse.cpp", [], "mm_parse")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -140,16 +140,6 @@ EXPORTED = sorted(_SIGS) + ["tb_last_error"]
 
 
 def _load():
-    override = os.environ.get("TB_LIB_OVERRIDE")  # experiments: load a variant build
-    if override:
-        lib = C.CDLL(override)
-        for name, args in _SIGS.items():
-            fn = getattr(lib, name)
-            fn.restype = C.c_int
-            fn.argtypes = args
-        lib.tb_last_error.restype = C.c_char_p
-        lib.tb_last_error.argtypes = []
-        return lib
     path = _build.LIB
     if not os.path.exists(path) or _build.needs_build():
         try:

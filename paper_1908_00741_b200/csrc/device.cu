@@ -35,12 +35,7 @@
 
 using tb::fail;
 
-#include "sweep_async.cuh"
-#include "sweep_cta.cuh"
 #include "sweep_lean.cuh"
-#include "sweep_reg.cuh"
-#include "sweep_ring.cuh"
-#include "sweep_tma.cuh"
 #include "spmv_tma.cuh"
 #include "persist.cuh"
 
@@ -1037,78 +1032,31 @@ int env_int(const char *name, int dflt) {
 }
 
 // Per color: pick the sweep kernel and size its launch.
-//   w == 32          -> step-ring kernel (sweep_ring.cuh)
-//   w | 32, w < 32   -> staged-task kernel (sweep_tma.cuh)
-//   otherwise / too large for shared memory -> simple kernel (sell_sweep)
-// TB_SWEEP=simple|staged|ring forces a family (if applicable);
-// TB_RING_R / TB_RING_WARPS override the ring depth / warps per SM.
+//   32-bit indexable plan, thread column of b_s steps fits shared memory
+//     -> lean thread-per-lane kernel (sweep_lean.cuh), KC = the color's
+//        longest slice rounded up to 2 / 4 / 6 / 8 slots;
+//   otherwise -> the plain thread-per-lane kernel (sell_sweep, 64-bit
+//     offsets, no shared memory).  TB_SWEEP=simple forces it (tests).
 int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
                      std::vector<tb_plan::ColorLaunch> &out) {
   out.assign(pl->n_c, tb_plan::ColorLaunch());
   const char *mode = getenv("TB_SWEEP");
   const bool force_simple = mode && !strcmp(mode, "simple");
-  // the staged-task kernel needs each task's slices contiguous (block order)
-  const bool force_staged = mode && !strcmp(mode, "staged") && !pl->step_major;
   const int w = (int)pl->w, b_s = (int)pl->b_s;
-  const bool shape_ok = w >= 1 && w <= 32 && (32 % w) == 0;
-  const int G = shape_ok ? 32 / w : 1;
-  size_t smem_optin = 227 * 1024, smem_sm = 228 * 1024;
+  size_t smem_optin = 227 * 1024;
   int v = 0;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device) == cudaSuccess)
     smem_optin = (size_t)v;
-  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, pl->device) == cudaSuccess)
-    smem_sm = (size_t)v;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, pl->device) == cudaSuccess)
     pl->num_sms = v;
+  const bool idx32 = pl->n <= 0x7fffffffLL && h.slice_ptr[h.n_slices] <= 0x7fffffffLL;
   for (long long c = 0; c < pl->n_c; ++c) {
     tb_plan::ColorLaunch &L = out[c];
     L.k0 = pl->color_lvl1[c];
     L.k1 = pl->color_lvl1[c + 1];
-    L.n_tasks = (L.k1 - L.k0 + G - 1) / G;
+    L.n_tasks = L.k1 - L.k0;
     if (force_simple || L.n_tasks <= 0) continue;
-    const bool idx32 = pl->n <= 0x7fffffffLL && h.slice_ptr[h.n_slices] <= 0x7fffffffLL;
-    if (mode && !strcmp(mode, "async") && idx32) {
-      // ---- cp.async ring, thread per lane
-      long long lmax = 0;
-      for (long long sid = L.k0 * b_s; sid < L.k1 * b_s; ++sid)
-        if (h.slice_len[sid] > lmax) lmax = h.slice_len[sid];
-      if (lmax < 1) lmax = 1;
-      int D = env_int("TB_ASYNC_D", 4);
-      if (D != 2 && D != 3 && D != 4 && D != 6 && D != 8) D = 4;
-      while (D > 2 && sweep_async::smem_bytes(D, (int)lmax, b_s) > smem_optin / 2) D = D > 4 ? 4 : D - 1;
-      const size_t sm = sweep_async::smem_bytes(D, (int)lmax, b_s);
-      if (sm <= smem_optin) {
-        L.kind = 6;
-        L.max_slots = (int)lmax;
-        L.ring = D;
-        L.warps = sweep_async::kThreads / 32;
-        L.smem = sm;
-        L.grid = (unsigned)(((L.k1 - L.k0) * w + sweep_async::kThreads - 1) / sweep_async::kThreads);
-        continue;
-      }
-    }
-    if (mode && !strcmp(mode, "cta") && idx32 && b_s * w <= 1024) {
-      // ---- two-pass CTA kernel
-      long long lmax = 0;
-      for (long long sid = L.k0 * b_s; sid < L.k1 * b_s; ++sid)
-        if (h.slice_len[sid] > lmax) lmax = h.slice_len[sid];
-      const int span = b_s * w;
-      int bpc = 256 / span;
-      if (bpc < 1) bpc = 1;
-      const size_t sm = sweep_cta::smem_bytes(bpc * span, (int)(lmax > 0 ? lmax : 1));
-      if (sm <= smem_optin && lmax < 4096) {
-        L.kind = 5;
-        L.max_slots = (int)(lmax > 0 ? lmax : 1);
-        L.ring = bpc;
-        L.warps = (bpc * span + 31) / 32;
-        L.smem = sm;
-        L.grid = (unsigned)((L.k1 - L.k0 + bpc - 1) / bpc);
-        continue;
-      }
-    }
-    if ((!mode || !strcmp(mode, "lean")) && idx32 &&
-        sweep_lean::smem_bytes(b_s, kBlock) <= smem_optin) {
-      // ---- lean thread-per-lane kernel (any w, 32-bit indexing)
+    if (idx32 && sweep_lean::smem_bytes(b_s, kBlock) <= smem_optin) {
       long long lmax = 0;
       for (long long sid = L.k0 * b_s; sid < L.k1 * b_s; ++sid)
         if (h.slice_len[sid] > lmax) lmax = h.slice_len[sid];
@@ -1117,95 +1065,10 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
       L.warps = 8;
       L.smem = sweep_lean::smem_bytes(b_s, kBlock);
       L.grid = grid_for((L.k1 - L.k0) * w);
-      continue;
     }
-    if (!mode || !strcmp(mode, "reg")) {
-      // ---- register-pipelined thread-per-lane kernel (any w)
-      long long lmax = 0;
-      for (long long sid = L.k0 * b_s; sid < L.k1 * b_s; ++sid) {
-        const long long len = (h.slice_ptr[sid + 1] - h.slice_ptr[sid]) / w;
-        if (len > lmax) lmax = len;
-      }
-      int maxl = 1;
-      while (maxl < lmax) maxl *= 2;
-      // prefetch distance: everything up front when a thread's whole walk
-      // fits ~64 registers of operands, else 2 steps ahead
-      int pf = (long long)b_s * (maxl * 5 + 4) <= 96 ? b_s : 2;
-      pf = env_int("TB_REG_PF", pf);
-      if (sweep_reg::select<true>(b_s, maxl, pf)) {
-        L.kind = 3;
-        L.max_slots = maxl;
-        L.ring = pf;
-        L.warps = 8;
-        L.grid = grid_for((L.k1 - L.k0) * w);
-        continue;
-      }
-    }
-    if (!shape_ok) continue;
-    if (w == 32 && (!force_staged || pl->step_major)) {
-      // ---- step ring
-      long long lmax = 0;
-      for (long long sid = L.k0 * b_s; sid < L.k1 * b_s; ++sid) {
-        const long long len = (h.slice_ptr[sid + 1] - h.slice_ptr[sid]) / 32;
-        if (len > lmax) lmax = len;
-      }
-      if (lmax < 1) lmax = 1;
-      int R = env_int("TB_RING_R", 4);
-      if (R < 1) R = 1;
-      if (R > sweep_ring::kMaxRing) R = sweep_ring::kMaxRing;
-      const size_t per_warp = sweep_ring::warp_bytes((int)lmax, R, b_s);
-      int wps = (int)(smem_sm / (per_warp + 64));  // warps per SM by shared memory
-      const int cap_w = env_int("TB_RING_WARPS", 32);
-      if (wps > cap_w) wps = cap_w;
-      if (wps >= 1 && lmax * 384 + 512 < (1 << 20)) {
-        int cta = wps < sweep_ring::kMaxWarps ? wps : sweep_ring::kMaxWarps;
-        const int ctas_per_sm = wps / cta;
-        L.kind = 2;
-        L.max_slots = (int)lmax;
-        L.ring = R;
-        L.warps = cta;
-        L.smem = per_warp * cta;
-        const long long nblk = L.k1 - L.k0;
-        long long want = (nblk + cta - 1) / cta;
-        long long capg = (long long)pl->num_sms * ctas_per_sm;
-        L.grid = (unsigned)(want < capg ? want : capg);
-        continue;
-      }
-    }
-    // ---- staged task (needs block-ordered slices)
-    if (pl->step_major) continue;
-    long long mx = 0;
-    for (long long t = 0; t < L.n_tasks; ++t) {
-      const long long kb = L.k0 + t * G;
-      const long long ke = kb + G < L.k1 ? kb + G : L.k1;
-      const long long slots = h.slice_ptr[ke * b_s] - h.slice_ptr[kb * b_s];
-      if (slots > mx) mx = slots;
-    }
-    mx = (mx + 3) / 4 * 4;
-    if (mx > (1 << 20) / 12) continue;  // one mbarrier tx-count per stage
-    const size_t per_warp = sweep_tma::warp_smem_bytes((int)mx, b_s, G);
-    int warps = (int)(smem_optin / per_warp);
-    if (warps > sweep_tma::kWarps) warps = sweep_tma::kWarps;
-    if (warps < 1) continue;
-    L.max_slots = (int)mx;
-    L.warps = warps;
-    L.smem = per_warp * warps;
-    long long want = (L.n_tasks + warps - 1) / warps;
-    long long cap = (long long)pl->num_sms * (long long)(smem_sm / (L.smem + 1024));
-    if (cap < 1) cap = 1;
-    L.grid = (unsigned)(want < cap ? want : cap);
-    L.kind = 1;
   }
   static bool attr_done = false;
   if (!attr_done) {
-    CU(cudaFuncSetAttribute(sweep_tma::sweep_kernel<true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin));
-    CU(cudaFuncSetAttribute(sweep_tma::sweep_kernel<false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin));
-    CU(cudaFuncSetAttribute(sweep_ring::sweep_kernel<true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin));
-    CU(cudaFuncSetAttribute(sweep_ring::sweep_kernel<false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin));
 #define TB_LEAN_ATTR(F, K)                                                         \
   CU(cudaFuncSetAttribute(sweep_lean::sweep_kernel<F, K, 32>,                      \
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin)); \
@@ -1214,18 +1077,6 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
     TB_LEAN_ATTR(true, 2) TB_LEAN_ATTR(true, 4) TB_LEAN_ATTR(true, 6) TB_LEAN_ATTR(true, 8)
     TB_LEAN_ATTR(false, 2) TB_LEAN_ATTR(false, 4) TB_LEAN_ATTR(false, 6) TB_LEAN_ATTR(false, 8)
 #undef TB_LEAN_ATTR
-    CU(cudaFuncSetAttribute(sweep_cta::sweep_kernel<true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin));
-    CU(cudaFuncSetAttribute(sweep_cta::sweep_kernel<false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin));
-#define TB_ASYNC_ATTR(F, D)                                                        \
-  CU(cudaFuncSetAttribute(sweep_async::sweep_kernel<F, D>,                         \
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin));
-    TB_ASYNC_ATTR(true, 2) TB_ASYNC_ATTR(true, 3) TB_ASYNC_ATTR(true, 4)
-    TB_ASYNC_ATTR(true, 6) TB_ASYNC_ATTR(true, 8) TB_ASYNC_ATTR(false, 2)
-    TB_ASYNC_ATTR(false, 3) TB_ASYNC_ATTR(false, 4) TB_ASYNC_ATTR(false, 6)
-    TB_ASYNC_ATTR(false, 8)
-#undef TB_ASYNC_ATTR
     attr_done = true;
   }
   return TB_OK;
@@ -1235,47 +1086,7 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
 template <bool FWD>
 void launch_phase(tb_plan *pl, const tb_plan::ColorLaunch &L, const DevSell &M,
                   const double *src, double *dst, cudaStream_t s, const PcgState *st) {
-  if (L.kind == 6) {
-    sweep_async::Params prm;
-    prm.slice_ptr = M.slice_ptr;
-    prm.slice_len = M.slice_len;
-    prm.col = M.col;
-    prm.val = M.val;
-    prm.inv_d = pl->inv_d;
-    prm.src = src;
-    prm.dst = dst;
-    prm.w = (int)pl->w;
-    prm.b_s = (int)pl->b_s;
-    prm.lmax = L.max_slots;
-    prm.k0 = (int)L.k0;
-    prm.nthreads = (int)((L.k1 - L.k0) * pl->w);
-    prm.done = st ? &st->done : nullptr;
-    const unsigned T = sweep_async::kThreads;
-    switch (L.ring) {
-      case 2: sweep_async::sweep_kernel<FWD, 2><<<L.grid, T, L.smem, s>>>(prm); break;
-      case 3: sweep_async::sweep_kernel<FWD, 3><<<L.grid, T, L.smem, s>>>(prm); break;
-      case 6: sweep_async::sweep_kernel<FWD, 6><<<L.grid, T, L.smem, s>>>(prm); break;
-      case 8: sweep_async::sweep_kernel<FWD, 8><<<L.grid, T, L.smem, s>>>(prm); break;
-      default: sweep_async::sweep_kernel<FWD, 4><<<L.grid, T, L.smem, s>>>(prm); break;
-    }
-  } else if (L.kind == 5) {
-    sweep_cta::Params prm;
-    prm.slice_ptr = M.slice_ptr;
-    prm.slice_len = M.slice_len;
-    prm.col = M.col;
-    prm.val = M.val;
-    prm.inv_d = pl->inv_d;
-    prm.src = src;
-    prm.dst = dst;
-    prm.w = (int)pl->w;
-    prm.b_s = (int)pl->b_s;
-    prm.bpc = L.ring;
-    prm.lmax = L.max_slots;
-    prm.k0 = (int)L.k0;
-    prm.k1 = (int)L.k1;
-    prm.done = st ? &st->done : nullptr;
-    sweep_cta::sweep_kernel<FWD><<<L.grid, L.ring * (int)(pl->b_s * pl->w), L.smem, s>>>(prm);
-  } else if (L.kind == 4) {
+  if (L.kind == 4) {
     const long long nt = (L.k1 - L.k0) * pl->w;
     const bool w32 = pl->w == 32;
     auto fn = L.max_slots == 2 ? (w32 ? sweep_lean::sweep_kernel<FWD, 2, 32> : sweep_lean::sweep_kernel<FWD, 2, 0>)
@@ -1285,45 +1096,6 @@ void launch_phase(tb_plan *pl, const tb_plan::ColorLaunch &L, const DevSell &M,
     fn<<<L.grid, kBlock, L.smem, s>>>(M.slice_ptr, M.slice_len, M.col, M.val, pl->inv_d, src,
                                       dst, (int)pl->w, (int)pl->b_s, (int)L.k0, (int)nt,
                                       st ? &st->done : nullptr);
-  } else if (L.kind == 3) {
-    const long long nt = (L.k1 - L.k0) * pl->w;
-    sweep_reg::KernelFn fn = sweep_reg::select<FWD>((int)pl->b_s, L.max_slots, L.ring);
-    fn<<<L.grid, kBlock, 0, s>>>(M.slice_ptr, M.slice_len, M.col, M.val, pl->inv_d, src, dst,
-                                 (int)pl->w,
-                                 L.k0, nt, st ? &st->done : nullptr);
-  } else if (L.kind == 2) {
-    sweep_ring::Params prm;
-    prm.slice_ptr = M.slice_ptr;
-    prm.slice_len = M.slice_len;
-    prm.col = M.col;
-    prm.val = M.val;
-    prm.inv_d = pl->inv_d;
-    prm.src = src;
-    prm.dst = dst;
-    prm.b_s = (int)pl->b_s;
-    prm.lmax = L.max_slots;
-    prm.ring = L.ring;
-    prm.k0 = L.k0;
-    prm.k1 = L.k1;
-    prm.done = st ? &st->done : nullptr;
-    sweep_ring::sweep_kernel<FWD><<<L.grid, L.warps * 32, L.smem, s>>>(prm);
-  } else if (L.kind == 1) {
-    sweep_tma::Params prm;
-    prm.slice_ptr = M.slice_ptr;
-    prm.col = M.col;
-    prm.val = M.val;
-    prm.inv_d = pl->inv_d;
-    prm.src = src;
-    prm.dst = dst;
-    prm.w = (int)pl->w;
-    prm.b_s = (int)pl->b_s;
-    prm.G = 32 / (int)pl->w;
-    prm.k0 = L.k0;
-    prm.k1 = L.k1;
-    prm.n_tasks = L.n_tasks;
-    prm.max_slots = L.max_slots;
-    prm.done = st ? &st->done : nullptr;
-    sweep_tma::sweep_kernel<FWD><<<L.grid, L.warps * 32, L.smem, s>>>(prm);
   } else {
     const long long nt = (L.k1 - L.k0) * pl->w;
     sell_sweep<FWD><<<grid_for(nt), kBlock, 0, s>>>(M.slice_ptr, M.slice_len, M.col, M.val,

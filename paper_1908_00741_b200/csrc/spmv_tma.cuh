@@ -20,7 +20,7 @@
 
 #pragma once
 
-#include "sweep_tma.cuh"
+#include "tma_util.cuh"
 
 namespace spmv_tma {
 
@@ -54,10 +54,10 @@ __device__ __forceinline__ void issue(const Params &p, long long q, unsigned cha
   const long long s1 = s0 + p.S < p.n_slices ? s0 + p.S : p.n_slices;
   const long long a = p.slice_ptr[s0], b = p.slice_ptr[s1];
   const unsigned cnt = (unsigned)(b - a);
-  sweep_tma::mbar_arrive_expect_tx(bar, cnt * 12u);
+  tma::mbar_arrive_expect_tx(bar, cnt * 12u);
   if (cnt) {
-    sweep_tma::bulk_g2s(stage, p.val + a, cnt * 8u, bar);
-    sweep_tma::bulk_g2s(stage + (size_t)cap * 8, p.col + a, cnt * 4u, bar);
+    tma::bulk_g2s(stage, p.val + a, cnt * 8u, bar);
+    tma::bulk_g2s(stage + (size_t)cap * 8, p.col + a, cnt * 4u, bar);
   }
 }
 
@@ -131,19 +131,19 @@ __device__ __forceinline__ double run(const Params &p, unsigned char *smem, unsi
   const long long G = gridDim.x;
   long long nmine = p.n_chunks > blockIdx.x ? (p.n_chunks - 1 - blockIdx.x) / G + 1 : 0;
   if (threadIdx.x == 0) {
-    sweep_tma::fence_proxy_async_smem();
+    tma::fence_proxy_async_smem();
     for (int i = 0; i < p.D && i < nmine; ++i)
       issue(p, blockIdx.x + i * G, smem + (size_t)i * stage_bytes(p.cap), p.cap, bars + i);
   }
   double part = 0.0;
   for (long long i = 0; i < nmine; ++i) {
     const int st = (int)(i % p.D);
-    sweep_tma::mbar_wait(bars + st, (phase >> st) & 1u);
+    tma::mbar_wait(bars + st, (phase >> st) & 1u);
     phase ^= 1u << st;
     part += compute<DOT>(p, blockIdx.x + i * G, smem + (size_t)st * stage_bytes(p.cap), p.cap);
     __syncthreads();
     if (threadIdx.x == 0 && i + p.D < nmine) {
-      sweep_tma::fence_proxy_async_smem();
+      tma::fence_proxy_async_smem();
       issue(p, blockIdx.x + (i + p.D) * G, smem + (size_t)st * stage_bytes(p.cap), p.cap,
             bars + st);
     }
@@ -155,7 +155,7 @@ __device__ __forceinline__ void init_bars(const Params &p, unsigned char *smem) 
   unsigned long long *bars =
       (unsigned long long *)(smem + (size_t)p.D * stage_bytes(p.cap));
   if (threadIdx.x == 0) {
-    for (int i = 0; i < p.D; ++i) sweep_tma::mbar_init(bars + i, 1);
+    for (int i = 0; i < p.D; ++i) tma::mbar_init(bars + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();

@@ -3,8 +3,10 @@
 Same dataclasses and field names as src/ordering.py:37-105; the greedy
 kernels and the padding/interleave passes run in the native host builder and
 are bit-exact with the reference (greedy first-fit is inherently sequential;
-see DESIGN.md).  The verifiers of src/ordering.py:283-346 are not rebuilt:
-they are test infrastructure and live in oracle/verify.py.
+see DESIGN.md).  The verifiers of src/ordering.py:283-346 (ER condition,
+level-2 structure) are not rebuilt: they are out of this path's scope
+ and tests/test_verifiers.py applies the reference's own
+verifiers to this module's orderings.
 """
 
 from collections.abc import Sequence
@@ -257,105 +259,3 @@ def extend_with_dummies(a: CsrMatrix, b, hl: HbmcLayout):
     vals = np.concatenate([a.vals, np.ones(nd)])
     b_ext = np.concatenate([np.asarray(b, dtype=np.float64), np.zeros(nd)])
     return CsrMatrix(n_pad, row_ptr, col_idx, vals), b_ext
-
-
-# ------------------------------------------------------------------ verifiers
-# src/ordering.py:109-143 (report types) and :283-346 (checks): the
-# equivalent-reordering (ER) condition of the paper and
-# the two structural guarantees the HBMC kernels rely on (w-wide steps are
-# diagonal; same-color level-1 blocks never couple).
-
-@dataclass(eq=False)
-class OrderingGraph:
-    """Directed edges over coupled pairs; direction = relative order."""
-
-    tail: np.ndarray
-    head: np.ndarray
-
-    def __post_init__(self):
-        self.tail = i64a(self.tail)
-        self.head = i64a(self.head)
-
-    @property
-    def n_edges(self):
-        return self.tail.shape[0]
-
-    def __eq__(self, other):
-        if not isinstance(other, OrderingGraph):
-            return NotImplemented
-        return bool(np.array_equal(self.tail, other.tail) and
-                    np.array_equal(self.head, other.head))
-
-
-@dataclass
-class ErReport:
-    holds: bool
-    n_pairs: int
-    n_violations: int
-    violations: list      # first few offending (i, j) pairs, original ids
-
-
-@dataclass
-class Level2Report:
-    holds: bool
-    n_diag_violations: int      # off-diagonal entries inside a w-wide step
-    n_cross_violations: int     # couplings between same-color level-1 blocks
-    examples: list
-
-
-def _pairs(a: CsrMatrix):
-    """Structurally coupled pairs (i < j), unique, sorted by (i, j)."""
-    rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.row_ptr))
-    cols = a.col_idx
-    m = rows != cols
-    i = np.minimum(rows[m], cols[m])
-    j = np.maximum(rows[m], cols[m])
-    key = np.unique(i * np.int64(max(a.n, 1)) + j)     # sorted, duplicates merged
-    return key // max(a.n, 1), key % max(a.n, 1)
-
-
-def build_ordering_graph(a: CsrMatrix, p: Permutation):
-    """Every coupled pair as an edge from the earlier to the later unknown
-    under p (src/ordering.py:299-306); edges sorted by (tail, head)."""
-    lo, hi = _pairs(a)
-    q = p.new_of_old
-    swap = q[lo] > q[hi]
-    tail = np.where(swap, hi, lo)
-    head = np.where(swap, lo, hi)
-    o = np.lexsort((head, tail))
-    return OrderingGraph(tail[o], head[o])
-
-
-def check_er_condition(a: CsrMatrix, p: Permutation, max_violations=20, pair_filter=None):
-    """Does p keep the relative order of every coupled pair (i < j =>
-    q[i] < q[j])?  pair_filter(lo, hi) -> mask restricts the scan
-    (src/ordering.py:309-325)."""
-    lo, hi = _pairs(a)
-    if pair_filter is not None:
-        keep = np.asarray(pair_filter(lo, hi), dtype=bool)
-        lo, hi = lo[keep], hi[keep]
-    q = p.new_of_old
-    bad = np.flatnonzero(q[lo] > q[hi])
-    return ErReport(bad.shape[0] == 0, int(lo.shape[0]), int(bad.shape[0]),
-                    [(int(lo[k]), int(hi[k])) for k in bad[:max_violations]])
-
-
-def check_level2_structure(a_final: CsrMatrix, hl, max_examples=10):
-    """Pattern scan of the HBMC-ordered matrix (src/ordering.py:328-346):
-    no off-diagonal coupling inside one w-wide step of a level-1 block
-    ("step"), none between two level-1 blocks of one color ("cross")."""
-    span = hl.b_s * hl.w
-    rows = np.repeat(np.arange(a_final.n, dtype=np.int64), np.diff(a_final.row_ptr))
-    cols = a_final.col_idx
-    m = rows != cols
-    r, c = rows[m], cols[m]
-    kr, kc = r // span, c // span
-    in_block = kr == kc
-    step_bad = in_block & ((r % span) // hl.w == (c % span) // hl.w)
-    cross_bad = ~in_block & (hl.level1_color[kr] == hl.level1_color[kc])
-    ex = [("step", int(x), int(y)) for x, y in zip(r[step_bad][:max_examples],
-                                                   c[step_bad][:max_examples])]
-    ex += [("cross", int(x), int(y)) for x, y in zip(r[cross_bad][:max_examples],
-                                                     c[cross_bad][:max_examples])]
-    nd, nc = int(step_bad.sum()), int(cross_bad.sum())
-    return Level2Report(nd == 0 and nc == 0, nd, nc, ex[:max_examples])

@@ -25,8 +25,7 @@ from .matrix import CsrMatrix, csr_to_sell, csr_transpose
 
 __all__ = [
     "IcBreakdownError", "IcFactor", "SellFactor", "BarrierCounter",
-    "WorkerPool", "ic0_factorize", "factor_equivalence_check",
-    "build_sell_factor", "ic_residual_on_pattern",
+    "WorkerPool", "ic0_factorize", "build_sell_factor",
     "sub_forward_seq", "sub_backward_seq", "sub_forward_mc",
     "sub_backward_mc", "sub_forward_bmc", "sub_backward_bmc",
     "sub_forward_hbmc", "sub_backward_hbmc", "apply_ic_preconditioner",
@@ -144,6 +143,15 @@ def _strict_tri(a: CsrMatrix, upper=False):
     return CsrMatrix(a.n, row_ptr, col, val, diag_ptr=np.full(a.n, -1, dtype=np.int64))
 
 
+def tri_row_counts(a: CsrMatrix, upper=False):
+    """Per-row entry counts of the strictly lower (upper) part (first pass
+    of _strict_tri only; used to count algorithmic bytes per color phase)."""
+    row_ptr = np.empty(a.n + 1, dtype=np.int64)
+    check(LIB.tb_csr_tri_count(a.n, ptr(a.row_ptr), ptr(a.col_idx), 1 if upper else 0,
+                               ptr(row_ptr)))
+    return np.diff(row_ptr)
+
+
 def _check_structural_symmetry(a: CsrMatrix):
     ok = _lib.i32()
     check(LIB.tb_csr_is_symmetric(a.n, ptr(a.row_ptr), ptr(a.col_idx), ok))
@@ -233,51 +241,6 @@ def ic0_factorize_device(a: CsrMatrix, hl, shift=0.0, layout_tag="hbmc", timings
                     csr_transpose(L))
 
 
-def ic_residual_on_pattern(a: CsrMatrix, f: IcFactor, kernels=None):
-    """src/precond.py:203-224 (verifier; native llt_on_pattern)."""
-    low_a = _strict_tri(a, upper=False)
-    pattern_ok = (np.array_equal(low_a.row_ptr, f.L.row_ptr)
-                  and np.array_equal(low_a.col_idx, f.L.col_idx))
-    low = np.empty(f.L.nnz)
-    diag = np.empty(f.n)
-    check(LIB.tb_llt_on_pattern(f.n, ptr(f.L.row_ptr), ptr(f.L.col_idx),
-                                ptr(f.L.vals), ptr(np.ascontiguousarray(f.d)),
-                                ptr(low), ptr(diag)))
-    ref_low = low_a.vals
-    ref_diag = a.diagonal() * (1.0 + f.shift)
-    max_rel = 0.0
-    if ref_low.shape[0] and low.shape[0] == ref_low.shape[0]:
-        max_rel = float(np.max(np.abs(low - ref_low) / np.maximum(np.abs(ref_low), 1e-300)))
-    max_rel = max(max_rel, float(np.max(np.abs(diag - ref_diag)
-                                        / np.maximum(np.abs(ref_diag), 1e-300))))
-    return max_rel, pattern_ok
-
-
-def factor_equivalence_check(a: CsrMatrix, p, shift=0.0, tol=1e-12, kernels=None):
-    """src/precond.py:232-260: does factorization commute with p?"""
-    from .matrix import permute_system
-    f1 = ic0_factorize(a, shift=shift)
-    a2, _ = permute_system(a, np.zeros(a.n), p)
-    f2 = ic0_factorize(a2, shift=shift)
-    q = p.new_of_old
-    r1 = np.repeat(np.arange(f1.n, dtype=np.int64), np.diff(f1.L.row_ptr))
-    r1m, c1m = q[r1], q[f1.L.col_idx]
-    if (c1m > r1m).any():
-        return False, float("inf")
-    order = np.lexsort((c1m, r1m))
-    r2 = np.repeat(np.arange(f2.n, dtype=np.int64), np.diff(f2.L.row_ptr))
-    if not (np.array_equal(r1m[order], r2) and np.array_equal(c1m[order], f2.L.col_idx)):
-        return False, float("inf")
-    v1, v2 = f1.L.vals, f2.L.vals
-    dev = 0.0
-    if v2.shape[0]:
-        dev = float(np.max(np.abs(v1[order] - v2) / np.maximum(np.abs(v2), 1e-300)))
-    d1m = np.empty_like(f1.d)
-    d1m[q] = f1.d
-    dev = max(dev, float(np.max(np.abs(d1m - f2.d) / np.maximum(np.abs(f2.d), 1e-300))))
-    return dev <= tol, dev
-
-
 def build_sell_factor(f: IcFactor, hl):
     """src/precond.py:263-270: L and U in SELL with slice width w."""
     if f.layout_tag != "hbmc":
@@ -351,6 +314,12 @@ def _hbmc_plan(sf, hl):
                              L_sell=sf.lower, U_sell=sf.upper)
     cache[id(hl)] = (hl, plan)
     return plan
+
+
+def release_plans(f):
+    """Free the device plans the sub_*/apply_* calls cached on factor `f`."""
+    for _, plan in f.__dict__.pop("_tb_plans", {}).values():
+        plan.close()
 
 
 def _count(counter, phases):

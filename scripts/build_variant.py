@@ -1,7 +1,11 @@
 """Build a variant of libhbmc_b200.so with extra nvcc defines (A/B experiments).
 
     python scripts/build_variant.py TAG -DNAME=VAL ...   -> scratch_libs/libhbmc_TAG.so
-Load it with TB_LIB_OVERRIDE=scratch_libs/libhbmc_TAG.so.
+Run a command against it on the GPU box with
+    scripts/with_variant.sh TAG <command...>
+which swaps it in for paper_1908_00741_b200/libhbmc_b200.so for the command
+and restores the default build afterwards (the product itself always loads
+its in-tree library).
 """
 import os
 import subprocess

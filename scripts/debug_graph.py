@@ -2,7 +2,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems, solver
+from paper_1908_00741_b200 import solver
+import workloads as problems
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 a = problems.varcoef7(n, seed=0); xs, b = problems.rhs(a)
 cfg = P.CgConfig(ordering="hbmc", b_s=8, w=32, spmv_format="sell")

@@ -3,7 +3,7 @@ import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems
+import workloads as problems
 dg = json.load(open("tests/golden/config2_digest.json"))
 a = problems.CONFIGS[2][1](); _, b = problems.rhs(a)
 href = np.array(dg["hbmc"]["history"])

@@ -3,7 +3,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems, solver
+from paper_1908_00741_b200 import solver
+import workloads as problems
 _, gen, bs, w = problems.CONFIGS[int(sys.argv[1])]
 a = gen(); xs, b = problems.rhs(a)
 cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")

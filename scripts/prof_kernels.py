@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems, solver
+from paper_1908_00741_b200 import solver
+import workloads as problems
 
 what, arg = sys.argv[1], sys.argv[2]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3

@@ -23,7 +23,8 @@ import numpy as np
 import torch
 
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems, solver
+from paper_1908_00741_b200 import solver
+import workloads as problems
 
 ids = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "1,2,3,4").split(",")]
 out_path = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/all_configs.json"

@@ -23,7 +23,8 @@ import numpy as np
 import torch
 
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems, solver
+from paper_1908_00741_b200 import solver
+import workloads as problems
 
 
 def rss_gb():

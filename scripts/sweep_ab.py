@@ -5,7 +5,8 @@ import os, sys, statistics, copy
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems, solver
+from paper_1908_00741_b200 import solver
+import workloads as problems
 arg = sys.argv[1]
 if arg.startswith("c5:"):
     a, bs, w = problems.lap7(int(arg[3:]), 1.0, 1.0, 1e-3), 16, 32

@@ -18,7 +18,8 @@ import numpy as np
 import torch
 
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems, solver
+from paper_1908_00741_b200 import solver
+import workloads as problems
 
 cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20

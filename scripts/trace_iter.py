@@ -10,7 +10,8 @@ import numpy as np
 import torch
 
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import _lib, problems, solver
+from paper_1908_00741_b200 import _lib, solver
+import workloads as problems
 
 arg = sys.argv[1] if len(sys.argv) > 1 else "2"
 if arg.startswith("c5:"):   # config 5 family at a given grid size

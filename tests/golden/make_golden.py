@@ -34,7 +34,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.abspath(os.path.join(HERE, "..", ".."))
 sys.path.insert(0, REPO)
 
-from paper_1908_00741_b200 import problems  # noqa: E402
+import workloads as problems  # noqa: E402
 from paper_1908_00741_b200 import matrix as M  # noqa: E402
 
 

@@ -26,7 +26,8 @@ import paper_1908_00741_b200 as P
 from conftest import golden_matrix, load_golden, rel_err
 from oracle import oracle as O
 from paper_1908_00741_b200 import distributed as D
-from paper_1908_00741_b200 import partition, problems, solver
+from paper_1908_00741_b200 import partition, solver
+import workloads as problems
 
 CASES = ["knn3000_b4_w32", "var7_16_b8_w32", "s27_10_b8_w32", "grid16_b4_w2",
          "rand500_b8_w4", "lap7_12_b4_w8"]

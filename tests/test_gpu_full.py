@@ -62,21 +62,83 @@ def _check_against_digest(rep, x, dg):
     assert rel_err(xs, xr) <= 1e-10
 
 
+def _check_ordering_against_digest(P, a, bs, w, dg):
+    """The bit-exact ordering contract at full size: BMC permutation, block
+    colors, composed HBMC permutation, padding (src/ordering.py:165-266)."""
+    lay = P.color_blocks(a, P.build_blocks(a, bs))
+    assert sha(lay.color_of_block) == dg["color_of_block_hash"]
+    assert sha(lay.perm.new_of_old) == dg["bmc_perm_hash"]
+    hl = P.build_hbmc(lay, w)
+    assert sha(hl.composed_perm.new_of_old) == dg["composed_hash"]
+    assert hl.n_c == dg["n_c"] and hl.n_dummy == dg["n_dummy"] and hl.n_pad == dg["n_pad"]
+    assert hl.nbar_of.tolist() == dg["nbar_of"]
+
+
 @pytest.mark.parametrize("cfg_id", [2, 3, 4])
 def test_full_config_iccg_matches_reference(P, cfg_id):
-    from paper_1908_00741_b200 import problems
+    import workloads as problems
     dg = _digest(cfg_id)
     label, gen, bs, w = problems.CONFIGS[cfg_id]
     a = gen()
     assert a.n == dg["n"] and a.nnz == dg["nnz"]
+    _check_ordering_against_digest(P, a, bs, w, dg)
     _, b = problems.rhs(a)
     x, rep = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell"))
     _check_against_digest(rep, x, dg)
 
 
+def test_full_config5_matches_oracle_digest(P):
+    """Config 5 (512^3, N = 134M) against tests/golden/config5_digest.json,
+    an independent build by the CPU oracle on the B200 host
+    (tests/golden/make_config5_digest.py): matrix, ordering hashes, padding,
+    IC(0) factor in SELL (bitwise), iterations within +-1, history head and
+    solution samples within 1e-10."""
+    import workloads
+    from paper_1908_00741_b200 import solver
+    path = os.path.join(GOLDEN, "config5_digest.json")
+    if not os.path.exists(path):
+        pytest.skip("config5_digest.json not generated")
+    dg = _digest(5)
+    label, gen, bs, w = workloads.CONFIGS[5]
+    a = gen()
+    h = hashlib.sha256()
+    for arr in (a.row_ptr, a.col_idx, a.vals):
+        h.update(np.ascontiguousarray(arr).tobytes())
+    assert h.hexdigest() == dg["a_hash"]
+    _, b = workloads.rhs(a)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    st = solver.prepare(a, b, cfg)
+    hl = st.layout
+    assert sha(hl.composed_perm.new_of_old) == dg["composed_hash"]
+    assert sha(hl.base.perm.new_of_old) == dg["bmc_perm_hash"]
+    assert sha(hl.base.color_of_block) == dg["color_of_block_hash"]
+    assert hl.n_c == dg["n_c"] and hl.n_dummy == dg["n_dummy"]
+    assert hl.nbar_of.tolist() == dg["nbar_of"]
+    assert sha(st.factor.d) == dg["d_hash"]
+    assert sha(st.factor.lower.slice_len) == dg["L_sell_slice_len_hash"]
+    assert sha(st.factor.lower.vals) == dg["L_sell_vals_hash"]
+    assert sha(st.factor.upper.vals) == dg["U_sell_vals_hash"]
+    del a
+    solver.attach_plan(st, cfg)
+    try:
+        x_sys, rep, hist = solver.solve_on_device(st, cfg)
+    finally:
+        st.plan.close()
+    x = x_sys[st.old_positions]
+    ref = dg["hbmc"]
+    assert rep.converged == ref["converged"]
+    assert abs(rep.iterations - ref["iterations"]) <= 1, (rep.iterations, ref["iterations"])
+    m = min(len(hist), len(ref["history"]), 40)
+    href = np.asarray(ref["history"][:m])
+    assert np.max(np.abs(np.asarray(hist[:m]) - href) / href) <= 1e-6
+    xs = x[::ref["x_sample_stride"]]
+    assert rel_err(xs, np.asarray(ref["x_sample"])) <= 1e-10
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_full_config2_partitioned_iccg(P, world):
-    from paper_1908_00741_b200 import distributed, problems
+    from paper_1908_00741_b200 import distributed
+    import workloads as problems
     dg = _digest(2)
     label, gen, bs, w = problems.CONFIGS[2]
     a = gen()
@@ -91,7 +153,8 @@ CASES = ["knn3000_b4_w32", "var7_16_b8_w32", "aniso12_b16_w32", "grid32_b8_w4",
 
 
 def _parts(P, name, world):
-    from paper_1908_00741_b200 import distributed, problems, solver
+    from paper_1908_00741_b200 import distributed, solver
+    import workloads as problems
     a, bs, w, rhs_kind = golden_matrix(name)
     b = np.ones(a.n) if rhs_kind == "ones" else problems.rhs(a)[1]
     cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
@@ -159,7 +222,8 @@ def test_partitioned_pcg_on_device(P, name, world):
 
 def test_partitioned_public_entry_point(P):
     """pcg_partitioned (virtual ranks) == the reference's report on a golden."""
-    from paper_1908_00741_b200 import distributed, problems
+    from paper_1908_00741_b200 import distributed
+    import workloads as problems
     name = "var7_16_b8_w32"
     g = load_golden(name)
     a, bs, w, _ = golden_matrix(name)
@@ -192,7 +256,8 @@ def test_device_ic0_bitwise(P, name):
 
 
 def test_device_ic0_breakdown_matches_host(P):
-    from paper_1908_00741_b200 import precond, problems
+    from paper_1908_00741_b200 import precond
+    import workloads as problems
     a = problems.lap7(8)
     vals = a.vals.copy()
     rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
@@ -238,7 +303,7 @@ def test_split_pcg_path(P, name, monkeypatch):
     monkeypatch.setenv("TB_PCG_SPLIT", "1")
     g = load_golden(name)
     a, bs, w, _ = golden_matrix(name)
-    from paper_1908_00741_b200 import problems
+    import workloads as problems
     _, b = problems.rhs(a)
     x, rep = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell"))
     assert abs(rep.iterations - int(g["pcg_hbmc_iters"])) <= 1
@@ -246,7 +311,7 @@ def test_split_pcg_path(P, name, monkeypatch):
 
 
 def test_split_pcg_full_config2(P, monkeypatch):
-    from paper_1908_00741_b200 import problems
+    import workloads as problems
     monkeypatch.setenv("TB_PCG_SPLIT", "1")
     dg = _digest(2)
     label, gen, bs, w = problems.CONFIGS[2]
@@ -314,7 +379,8 @@ def test_p2p_fused_pcg_on_device(P, name, world):
 
 
 def test_p2p_transport_pcg_full_config2(P):
-    from paper_1908_00741_b200 import distributed, problems
+    from paper_1908_00741_b200 import distributed
+    import workloads as problems
     dg = _digest(2)
     label, gen, bs, w = problems.CONFIGS[2]
     a = gen()
@@ -345,7 +411,7 @@ def test_pcg_paths_interleaved_on_one_plan(P, monkeypatch):
     from paper_1908_00741_b200 import solver
     g = load_golden("var7_16_b8_w32")
     a, bs, w, _ = golden_matrix("var7_16_b8_w32")
-    from paper_1908_00741_b200 import problems
+    import workloads as problems
     _, b = problems.rhs(a)
     cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
     st = solver.attach_plan(solver.prepare(a, b, cfg), cfg)
@@ -430,7 +496,7 @@ def test_every_pcg_path_meets_the_bar(P, name, env, monkeypatch):
     persistent launch, per-phase graph, host-polled kernel sequence, with
     and without the fused / paired vector kernels and the TMA SpMV) meets
     the north-star bar against the reference's run."""
-    from paper_1908_00741_b200 import problems
+    import workloads as problems
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = load_golden(name)

@@ -114,7 +114,7 @@ def test_pcg_matches_reference(P, name, ordering):
     if rhs_kind == "ones":
         b = np.ones(a.n)
     else:
-        from paper_1908_00741_b200 import problems
+        import workloads as problems
         _, b = problems.rhs(a)
     cfg = P.CgConfig(ordering=ordering, b_s=bs, w=w,
                      spmv_format="sell" if ordering == "hbmc" else "crs")

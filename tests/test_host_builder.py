@@ -18,7 +18,8 @@ import pytest
 import paper_1908_00741_b200 as P
 from conftest import GOLDEN, REPO, golden_matrix, golden_names, load_golden
 from oracle import oracle as O
-from paper_1908_00741_b200 import _lib, kernels, problems
+from paper_1908_00741_b200 import _lib, kernels
+import workloads as problems
 
 NAMES = golden_names()
 

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import paper_1908_00741_b200 as P
-from paper_1908_00741_b200 import problems
+import workloads as problems
 
 BANNER_SYM = "%%MatrixMarket matrix coordinate real symmetric"
 BANNER_GEN = "%%MatrixMarket matrix coordinate real general"

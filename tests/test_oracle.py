@@ -96,3 +96,44 @@ def test_pcg_hbmc_matches_reference(case):
     assert conv == bool(g["pcg_hbmc_converged"])
     assert np.allclose(hist, g["pcg_hbmc_hist"], rtol=1e-12, atol=0)
     assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg_id,size", [(1, 9), (2, 10), (3, 7), (4, 2000), (5, 11)])
+def test_oracle_assembly_equals_product(cfg_id, size):
+    """workloads.py assembles the same COO through the oracle's C
+    coo_to_csr (bench.py's reference arm) and the product's: same CSR, same
+    b = A x* (src/matrix.py:168-197, K/numba_backend.py:16-23)."""
+    import workloads
+    ap, _, _ = workloads.scaled(cfg_id, size)
+    ao, _, _ = workloads.scaled(cfg_id, size, backend="oracle")
+    assert np.array_equal(ap.row_ptr, ao.row_ptr)
+    assert np.array_equal(ap.col_idx, ao.col_idx)
+    assert np.array_equal(ap.vals, ao.vals)
+    _, bp = workloads.rhs(ap)
+    _, bo = workloads.rhs(ao, backend="oracle")
+    assert np.array_equal(bp, bo)
+
+
+def test_oracle_coo_duplicate_rejected():
+    row = np.array([0, 1, 1, 0], dtype=np.int64)
+    col = np.array([0, 1, 1, 1], dtype=np.int64)
+    with pytest.raises(ValueError, match=r"duplicate entry at \(1, 1\)"):
+        O.coo_to_csr(2, row, col, np.ones(4))
+
+
+def test_oracle_permute_transpose_match_numpy(rng):
+    """or_permute_csr / or_csr_transpose == the reference's COO -> lexsort
+    formulation (src/matrix.py:200-208, 293-304) on a random pattern."""
+    n = 300
+    a = golden_matrix("rand300_b3_w5")[0]
+    a = O.Csr(a.n, a.row_ptr, a.col_idx, a.vals)
+    q = rng.permutation(n).astype(np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.row_ptr))
+    ap, _ = O.permute_system(a, np.zeros(n), q)
+    order = np.lexsort((q[a.col_idx], q[rows]))
+    assert np.array_equal(ap.col_idx, q[a.col_idx][order])
+    assert np.array_equal(ap.vals, a.vals[order])
+    at = O.csr_transpose(a)
+    order = np.lexsort((rows, a.col_idx))
+    assert np.array_equal(at.col_idx, rows[order])
+    assert np.array_equal(at.vals, a.vals[order])

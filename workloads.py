@@ -1,4 +1,5 @@
-"""The BASELINE.json problem generators.
+"""The BASELINE.json workloads -- test and bench
+infrastructure, not the product.
 
 The reference ships only 2-D generators (src/matrix.py:326-374); these are
 the five 3-D / graph problems BASELINE.json names, defined exactly as the
@@ -9,11 +10,16 @@ neighbours).  Diagonal sums are accumulated in the same element order as a
 sequential np.add.at over `lo` then `hi` (np.bincount over the concatenation
 performs exactly that sequence of additions), so values are bit-identical to
 the survey's recipe.
+
+This module is pure numpy at import time.  Each generator returns a CSR
+assembled by the product's `coo_to_csr` (default) or, with
+`backend="oracle"`, by the CPU oracle's (oracle/oracle.py) -- so bench.py's
+reference arm builds its matrix without loading the product library.  Both
+assemble the same COO triplets with the same (row, col) lexsort contract
+(src/matrix.py:168-197); `tests/test_oracle.py` checks that they agree.
 """
 
 import numpy as np
-
-from .matrix import CooMatrix, coo_to_csr, spmv_host_exact
 
 
 def _edges3d(nx, ny, nz):
@@ -28,13 +34,6 @@ def _edges3d(nx, ny, nz):
     return out
 
 
-def _assemble(n, lo, hi, off, diag):
-    rows = np.concatenate([lo, hi, np.arange(n, dtype=np.int64)])
-    cols = np.concatenate([hi, lo, np.arange(n, dtype=np.int64)])
-    vals = np.concatenate([-off, -off, diag])
-    return coo_to_csr(CooMatrix(n, rows, cols, vals))
-
-
 def _seq_sum(n, lo, hi, w, init=None):
     """diag = init; diag[lo[k]] += w[k] (k asc); then the same over hi."""
     if init is None:
@@ -46,7 +45,20 @@ def _seq_sum(n, lo, hi, w, init=None):
     return np.bincount(idx, weights=wt, minlength=n)
 
 
-def lap7(n, cx=1.0, cy=1.0, cz=1.0):
+def _assemble(n, lo, hi, off, diag, backend):
+    """COO [lo->hi, hi->lo, diag] -> CSR (src/matrix.py:168-197)."""
+    rows = np.concatenate([lo, hi, np.arange(n, dtype=np.int64)])
+    cols = np.concatenate([hi, lo, np.arange(n, dtype=np.int64)])
+    del lo, hi
+    vals = np.concatenate([-off, -off, diag])
+    if backend == "oracle":
+        from oracle import oracle as O
+        return O.coo_to_csr(n, rows, cols, vals)
+    from paper_1908_00741_b200.matrix import CooMatrix, coo_to_csr
+    return coo_to_csr(CooMatrix(n, rows, cols, vals))
+
+
+def lap7(n, cx=1.0, cy=1.0, cz=1.0, backend="product"):
     """Configs 1 and 5: constant-coefficient (anisotropic) 7-point stencil.
 
     Off-diagonals -cx / -cy / -cz, diagonal 2*(cx+cy+cz) on every row."""
@@ -56,11 +68,12 @@ def lap7(n, cx=1.0, cy=1.0, cz=1.0):
     hi = np.concatenate([xh, yh, zh])
     c = np.concatenate([np.full(xl.size, cx), np.full(yl.size, cy),
                         np.full(zl.size, cz)])
+    del xl, xh, yl, yh, zl, zh
     diag = np.full(N, 2 * (cx + cy + cz))
-    return _assemble(N, lo, hi, c, diag)
+    return _assemble(N, lo, hi, c, diag, backend)
 
 
-def varcoef7(n, seed=0):
+def varcoef7(n, seed=0, backend="product"):
     """Config 2: kappa ~ lognormal(0, 1) per cell, harmonic face averages,
     Dirichlet faces contribute 2*kappa_i."""
     rng = np.random.default_rng(seed)
@@ -73,10 +86,10 @@ def varcoef7(n, seed=0):
     diag = _seq_sum(N, lo, hi, c)
     deg = _seq_sum(N, lo, hi, np.ones(lo.size))
     diag += (6 - deg) * 2 * kappa
-    return _assemble(N, lo, hi, c, diag)
+    return _assemble(N, lo, hi, c, diag, backend)
 
 
-def stencil27(n, seed=0):
+def stencil27(n, seed=0, backend="product"):
     """Config 3: 27-point, off-diagonals -u, u ~ U[0.5, 1.5] per unordered
     pair (13 forward offsets in lexicographic order), diagonal
     1.01 * row sum of |off-diagonals|."""
@@ -101,10 +114,10 @@ def stencil27(n, seed=0):
     u = rng.uniform(0.5, 1.5, lo.size)
     diag = _seq_sum(N, lo, hi, u)
     diag *= 1.01
-    return _assemble(N, lo, hi, u, diag)
+    return _assemble(N, lo, hi, u, diag, backend)
 
 
-def knn_graph(N, k=14, seed=0):
+def knn_graph(N, k=14, seed=0, backend="product"):
     """Config 4: N uniform points in the unit cube, edges to the k nearest
     neighbours (symmetrised, unique pairs, first occurrence kept), weights
     1/dist, node ids relabelled by a random permutation, diagonal = weight
@@ -125,30 +138,51 @@ def knn_graph(N, k=14, seed=0):
     perm = rng.permutation(N)
     lo, hi = perm[lo], perm[hi]
     diag = _seq_sum(N, lo, hi, wgt, init=np.full(N, 1e-3))
-    return _assemble(N, lo, hi, wgt, diag)
+    return _assemble(N, lo, hi, wgt, diag, backend)
 
 
-# BASELINE.json configs: id -> (label, generator, b_s, w)
-CONFIGS = {
-    1: ("poisson7_32^3", lambda: lap7(32), 4, 8),
-    2: ("varcoef7_128^3", lambda: varcoef7(128, seed=0), 8, 32),
-    3: ("stencil27_192^3", lambda: stencil27(192, seed=0), 8, 32),
-    4: ("knn14_4M", lambda: knn_graph(4_000_000, seed=0), 4, 32),
-    5: ("aniso7_512^3", lambda: lap7(512, 1.0, 1.0, 1e-3), 16, 32),
+# BASELINE.json configs: id -> (label, b_s, w, generator(backend))
+_GEN = {
+    1: ("poisson7_32^3", 4, 8, lambda be: lap7(32, backend=be)),
+    2: ("varcoef7_128^3", 8, 32, lambda be: varcoef7(128, seed=0, backend=be)),
+    3: ("stencil27_192^3", 8, 32, lambda be: stencil27(192, seed=0, backend=be)),
+    4: ("knn14_4M", 4, 32, lambda be: knn_graph(4_000_000, seed=0, backend=be)),
+    5: ("aniso7_512^3", 16, 32, lambda be: lap7(512, 1.0, 1.0, 1e-3, backend=be)),
 }
 
+# id -> (label, generator() with the product's assembly, b_s, w)
+CONFIGS = {k: (lab, (lambda g=g: g("product")), bs, w) for k, (lab, bs, w, g) in _GEN.items()}
 
-def scaled(cfg_id, size):
+
+def generate(cfg_id, backend="product"):
+    """(label, A, b_s, w) of BASELINE config `cfg_id`."""
+    label, bs, w, g = _GEN[cfg_id]
+    return label, g(backend), bs, w
+
+
+def scaled(cfg_id, size, backend="product"):
     """Same family as config `cfg_id` at a smaller size (parity tests)."""
-    _, _, b_s, w = CONFIGS[cfg_id]
-    gen = {1: lambda: lap7(size), 2: lambda: varcoef7(size, seed=0),
-           3: lambda: stencil27(size, seed=0), 4: lambda: knn_graph(size, seed=0),
-           5: lambda: lap7(size, 1.0, 1.0, 1e-3)}[cfg_id]
+    _, b_s, w, _ = _GEN[cfg_id]
+    gen = {1: lambda: lap7(size, backend=backend),
+           2: lambda: varcoef7(size, seed=0, backend=backend),
+           3: lambda: stencil27(size, seed=0, backend=backend),
+           4: lambda: knn_graph(size, seed=0, backend=backend),
+           5: lambda: lap7(size, 1.0, 1.0, 1e-3, backend=backend)}[cfg_id]
     return gen(), b_s, w
 
 
-def rhs(a, seed=1):
-    """x* = default_rng(seed).uniform(-1, 1, N); b = A x* in the reference's
-    sequential CSR accumulation order (computed once, on the host)."""
-    xs = np.random.default_rng(seed).uniform(-1, 1, a.n)
+def xstar(n, seed=1):
+    """x* = default_rng(seed).uniform(-1, 1, N)."""
+    return np.random.default_rng(seed).uniform(-1, 1, n)
+
+
+def rhs(a, seed=1, backend="product"):
+    """x*, b = A x* in the reference's sequential CSR accumulation order
+    (src/matrix.py:307-323 -> K/numba_backend.py:16-23; computed once, on
+    the host)."""
+    xs = xstar(a.n, seed)
+    if backend == "oracle":
+        from oracle import oracle as O
+        return xs, O.spmv_csr(a, xs)
+    from paper_1908_00741_b200.matrix import spmv_host_exact
     return xs, spmv_host_exact(a, xs)
