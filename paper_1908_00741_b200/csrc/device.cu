@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(spmv_tma::kThreads, 2)
   // x/r over the rows of this CTA's chunks (the rows run<> produced)
   double rr = 0.0;
   const long long rows_per_chunk = (long long)p.S * 32;
-  const long long n = p.n_slices * 32;
+  const long long n = p.n;
   for (long long q = blockIdx.x; q < p.n_chunks; q += gridDim.x) {
     const long long r0 = q * rows_per_chunk;
     const long long r1 = r0 + rows_per_chunk < n ? r0 + rows_per_chunk : n;
@@ -1154,6 +1154,7 @@ int launch_backward(tb_plan *pl, const double *src, double *dst, cudaStream_t s,
 }
 
 void spmv_params(const tb_plan *pl, const double *x, double *out, spmv_tma::Params &P) {
+  P.n = pl->n;
   P.n_slices = pl->A.n_slices;
   P.slice_ptr = pl->A.slice_ptr;
   P.slice_len = pl->A.slice_len;
@@ -1337,6 +1338,29 @@ void drop_graph(tb_plan *pl) {
 // Access-policy window over the CG vector pool on pl->stream (on) or none
 // (off).  The persisting set-aside is the device maximum; the hit ratio
 // scales the window down to it.
+// Scope guard for the persisting-L2 set-aside of a solve: raise() records
+// the device's current limit and sets the new one; the destructor drops the
+// persisting lines and restores the recorded limit (every exit path of
+// tb_pcg, including CU() early returns).  Process-wide while it lives --
+// see INTEGRATION.md.
+struct L2SetAside {
+  bool active = false;
+  size_t prev = 0;
+  void raise(size_t bytes) {
+    if (cudaDeviceGetLimit(&prev, cudaLimitPersistingL2CacheSize) == cudaSuccess &&
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) == cudaSuccess)
+      active = true;
+    else
+      cudaGetLastError();
+  }
+  ~L2SetAside() {
+    if (!active) return;
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev);
+    cudaGetLastError();
+  }
+};
+
 void set_l2_window(tb_plan *pl, bool on) {
   cudaStreamAttrValue v;
   memset(&v, 0, sizeof(v));
@@ -1347,10 +1371,12 @@ void set_l2_window(tb_plan *pl, bool on) {
     const long long nv = pl->n > 0 ? pl->n : 1;
     size_t bytes = sizeof(double) * (size_t)(5 * ((nv + 31) / 32 * 32));
     if (max_win <= 0 || max_persist <= 0) return;
-    // only where most of the pool fits the set-aside: config 2 (84 MB of
-    // vectors) 21.8 vs 22.5 ms; config 3 (283 MB) 54.8 vs 51.5 ms, the
-    // set-aside then only takes L2 from the factor stream (profiles/README.md)
-    if (bytes > 2 * (size_t)max_persist || bytes > (size_t)max_win) return;
+    // only where the pool (nearly) fits the set-aside: config 2 (84 MB of
+    // vectors, 1.01x the set-aside) 21.8 vs 22.5 ms; config 3 (283 MB, 3.4x)
+    // 54.8 vs 51.5 ms -- the set-aside then only takes L2 from the factor
+    // stream (profiles/README.md).  Ratios between those two were not
+    // measured, so the gate stays at the measured gain (<= 1.25x).
+    if (bytes * 4 > 5 * (size_t)max_persist || bytes > (size_t)max_win) return;
     pl->l2_persist = (size_t)max_persist;
     v.accessPolicyWindow.base_ptr = pl->vec_pool;
     v.accessPolicyWindow.num_bytes = bytes;
@@ -1890,7 +1916,11 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
   pl->p = pl->z + nv_al;
   pl->ap = pl->p + nv_al;
   if ((rc = upload<double>(&pl->partials, nullptr, kMaxPartials))) return bail(rc);
-  // NaN-poison the work vectors: every kernel must write before it reads
+  // zero the pool (alignment gaps included: a slice-padded kernel may read
+  // past n), then NaN-poison the work vectors' rows: every kernel must
+  // write a row before it reads it
+  if (cudaMemset(pl->vec_pool, 0, sizeof(double) * (size_t)(5 * nv_al)) != cudaSuccess)
+    return bail(fail(TB_ECUDA, "plan_create: memset failed"));
   for (double *v : {pl->r, pl->y, pl->z, pl->p, pl->ap})
     if (cudaMemset(v, 0xff, sizeof(double) * (size_t)nv) != cudaSuccess)
       return bail(fail(TB_ECUDA, "plan_create: memset failed"));
@@ -2188,10 +2218,10 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
                          pl->stream));
     }
     // the persisting set-aside exists only while the solve runs: every other
-    // launch (sweeps, SpMV, callers' kernels) keeps the whole L2
-    if (pl->l2_window && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pl->l2_persist) !=
-                             cudaSuccess)
-      cudaGetLastError();
+    // launch (sweeps, SpMV, callers' kernels) keeps the whole L2.  The guard
+    // restores the caller's previous limit on every exit path.
+    L2SetAside l2guard;
+    if (pl->l2_window) l2guard.raise(pl->l2_persist);
     CU(cudaGraphLaunch(pl->gexec, pl->stream));
     CU(cudaMemcpyAsync(&hs, pl->st, sizeof(PcgState), cudaMemcpyDeviceToHost, pl->stream));
     if (pl->split_pcg)
@@ -2201,12 +2231,6 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
     // the last application may not have bumped (the loop stopped before its
     // p update): never reuse its epoch
     if (pl->split_pcg) ++pl->epoch;
-    // drop the persisting lines so later launches see a normal L2
-    if (pl->l2_window) {
-      cudaCtxResetPersistingL2Cache();
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-      cudaGetLastError();
-    }
   }
   pl->split_pcg = false;
   if ((rc = sync_out(pl, stream))) return rc;

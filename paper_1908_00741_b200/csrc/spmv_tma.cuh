@@ -29,6 +29,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kG = 8;   // gathers in flight per lane
 
 struct Params {
+  long long n;                 // rows (the last slice may hold rows >= n: skipped)
   long long n_slices;
   const long long *slice_ptr;  // element offsets, multiples of 32
   const int *slice_len;
@@ -109,12 +110,16 @@ __device__ __forceinline__ double compute(const Params &p, long long q,
     double acc0 = 0.0, acc1 = 0.0;
     rows2(sv, sc, off0, len0, off1, len1, p.x, acc0, acc1);
     const long long r0 = s * 32 + lane;
-    p.out[r0] = acc0;
-    if (DOT) part += __ldcg(p.x + r0) * acc0;
+    if (r0 < p.n) {
+      p.out[r0] = acc0;
+      if (DOT) part += __ldcg(p.x + r0) * acc0;
+    }
     if (two) {
       const long long r1 = t * 32 + lane;
-      p.out[r1] = acc1;
-      if (DOT) part += __ldcg(p.x + r1) * acc1;
+      if (r1 < p.n) {
+        p.out[r1] = acc1;
+        if (DOT) part += __ldcg(p.x + r1) * acc1;
+      }
     }
   }
   return part;

@@ -55,3 +55,39 @@ def test_tensor_in_tensor_out(P):
     yd = P.spmv(a, torch.from_numpy(x).cuda())
     assert isinstance(yd, torch.Tensor) and yd.is_cuda
     assert np.array_equal(yd.cpu().numpy(), P.spmv(a, x))
+
+
+def test_sell32_plan_spmv_n_not_multiple_of_32(P):
+    """A width-32 SELL A with n % 32 != 0 runs the TMA-staged plan SpMV: it
+    must write only rows < n (the caller's y has length n) and leave the
+    padded rows out of p.Ap -- the reference pads x to n_pad and returns
+    out[:n] (src/matrix.py:315-322)."""
+    import torch
+    from paper_1908_00741_b200 import solver
+    a = P.gen_random_spd(1000, density=0.01, seed=5)
+    cfg = P.CgConfig(ordering="natural", w=32, spmv_format="sell")
+    st = solver.attach_plan(solver.prepare(a, np.ones(a.n), cfg), cfg)
+    plan = st.plan
+    try:
+        x = torch.from_numpy(np.random.default_rng(0).standard_normal(a.n)).cuda()
+        buf = torch.full((a.n + 64,), 12345.0, dtype=torch.float64, device="cuda")
+        plan.spmv(x, buf[:a.n])
+        torch.cuda.synchronize()
+        out = buf.cpu().numpy()
+        assert np.all(out[a.n:] == 12345.0), "plan SpMV wrote past row n"
+        ref = P.spmv(a, x.cpu().numpy())
+        assert np.array_equal(out[:a.n], ref)
+    finally:
+        plan.close()
+
+
+def test_natural_sell32_solve_n_not_multiple_of_32(P):
+    """Whole solve through the TMA SpMV + fused p.Ap with n % 32 != 0
+    converges like the CRS solve (no NaN from the slice padding)."""
+    a = P.gen_random_spd(1000, density=0.01, seed=5)
+    b = np.ones(a.n)
+    x1, r1 = P.pcg(a, b, P.CgConfig(ordering="natural", w=32, spmv_format="sell"))
+    x2, r2 = P.pcg(a, b, P.CgConfig(ordering="natural", spmv_format="crs"))
+    assert r1.converged and r2.converged
+    assert abs(r1.iterations - r2.iterations) <= 1
+    assert np.linalg.norm(x1 - x2) <= 1e-10 * np.linalg.norm(x2)
