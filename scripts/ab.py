@@ -57,8 +57,15 @@ K, R = 10, 5
 ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
       for _ in range(K)]
 res = {name: [] for name, _ in plans}
-for _, pl in plans:
+zs = {}
+for name, pl in plans:
+    z.fill_(float("nan"))
     pl.precond(r, z)
+    torch.cuda.synchronize()
+    zs[name] = z.clone()
+z0 = zs[plans[0][0]]
+for name, _ in plans:
+    print(f"{name:14s} z bitwise vs {plans[0][0]}: {bool(torch.equal(zs[name], z0))}", flush=True)
 for rnd in range(R):
     for name, pl in plans:
         torch.cuda.synchronize()
