@@ -77,53 +77,53 @@ __device__ __forceinline__ void run(const persist::Params &P, unsigned char *sme
   const unsigned epoch = P.epoch_dev ? *P.epoch_dev : P.epoch;
   const double *src = P.pre_src;
   double *mid = P.y, *dst = P.pre_dst;
-  const size_t SB = slot_bytes(LC);
+  const unsigned SB = (unsigned)slot_bytes(LC);
   unsigned char *wb = smem + (size_t)wid * warp_bytes(LC, D, b_s);
+  const unsigned wb_s = s32(wb);   // shared-window address of the warp's ring
   double *ys = (double *)(wb + (size_t)D * SB);
   int *slen = (int *)(wb + (size_t)D * SB + (size_t)b_s * 256);
 
   // ---- issue side: descriptors (slice offset / length of every step) of
   // the item being issued (A) and the next one (B), lane l holding step l
   int iq = 0, ii = 0, islot = 0;
-  long long a_off = 0, b_off = 0;
-  int a_len = 0, b_len = 0;
-  auto load_desc = [&](int q, long long &off, int &len) {
+  int a_off = 0, b_off = 0, a_len = 0, b_len = 0;
+  auto load_desc = [&](int q, int &off, int &len) {
     const Item it = item_of(gw, q, W, n);
     off = 0;
     len = 0;
     if (it.valid && lane < b_s) {
       const int l = it.fwd ? lane : b_s - 1 - lane;
       const int sid = it.k * b_s + l;
-      off = it.fwd ? P.Lsp[sid] : P.Usp[sid];
+      off = (int)(it.fwd ? P.Lsp[sid] : P.Usp[sid]);
       len = it.fwd ? P.Lsl[sid] : P.Usl[sid];
     }
   };
   load_desc(0, a_off, a_len);
   load_desc(1, b_off, b_len);
-  // stream the static operands of the next step into ring slot islot; one
-  // commit group per step (empty past the last item)
+  // stream the static operands of the next step into ring slot islot: the
+  // slice's values (16 x len chunks of 16 B), columns (8 x len) and the 32
+  // inv_d (16); one commit group per step (empty past the last item)
   auto issue = [&]() {
     const Item it = item_of(gw, iq, W, n);
     if (it.valid) {
-      const int off = (int)__shfl_sync(FULL, a_off, ii);
+      const int off = __shfl_sync(FULL, a_off, ii);
       const int len = __shfl_sync(FULL, a_len, ii);
       const int l = it.fwd ? ii : b_s - 1 - ii;
-      const int row0 = (it.k * b_s + l) * 32;
-      unsigned char *sl = wb + (size_t)islot * SB;
-      const double *gv = (it.fwd ? P.Lval : P.Uval) + off;
-      const int *gc = (it.fwd ? P.Lcol : P.Ucol) + off;
-      const double *gi = P.inv_d + row0;
-      const int nv = 16 * len, nc = 8 * len, tot = nv + nc + 16;
-      for (int c = lane; c < tot; c += 32) {
-        if (c < nv)
-          cp16(sl + (size_t)c * 16, (const unsigned char *)gv + (size_t)c * 16);
-        else if (c < nv + nc)
-          cp16(sl + (size_t)LC * 256 + (size_t)(c - nv) * 16,
-               (const unsigned char *)gc + (size_t)(c - nv) * 16);
-        else
-          cp16(sl + (size_t)LC * 384 + (size_t)(c - nv - nc) * 16,
-               (const unsigned char *)gi + (size_t)(c - nv - nc) * 16);
-      }
+      const unsigned sl = wb_s + (unsigned)islot * SB;
+      const char *gv = (const char *)((it.fwd ? P.Lval : P.Uval) + off);
+      const char *gc = (const char *)((it.fwd ? P.Lcol : P.Ucol) + off);
+      for (int c = lane; c < 16 * len; c += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sl + c * 16),
+                     "l"(gv + c * 16) : "memory");
+      const unsigned slc = sl + (unsigned)LC * 256;
+      for (int c = lane; c < 8 * len; c += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slc + c * 16),
+                     "l"(gc + c * 16) : "memory");
+      if (lane < 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         sl + (unsigned)LC * 384 + lane * 16),
+                     "l"((const char *)(P.inv_d + (it.k * b_s + l) * 32) + lane * 16)
+                     : "memory");
       if (lane == 0) slen[islot] = len;
     }
     commit();
@@ -145,64 +145,53 @@ __device__ __forceinline__ void run(const persist::Params &P, unsigned char *sme
   for (int q = 0;; ++q) {
     const Item it = item_of(gw, q, W, n);
     if (!it.valid) break;
+    const bool fwd = it.fwd;
     const int k = it.k;
     const int span = b_s * 32, blk0 = k * span;
     const unsigned uspan = (unsigned)span;
-    const double *rhs_v = it.fwd ? src : mid;
-    double *out = it.fwd ? mid : dst;
-    if (it.fwd)
-      persist::wait_flags(P, P.fflag, P.fdep, P.fdep_ptr[k], P.fdep_ptr[k + 1], epoch);
+    const double *rhs_v = fwd ? src : mid;
+    double *out = fwd ? mid : dst;
+    if (fwd)
+      persist::wait_flags(P, P.fflag, P.fdep, P.fdep_ptr[k], P.fdep_ptr[k + 1], epoch,
+                          nullptr, P.s_ns);
     else
       persist::wait_flags(P, P.bflag, P.bdep, P.bdep_ptr[k], P.bdep_ptr[k + 1], epoch,
-                          P.fflag + k);
-    // dynamic operands of walk step i (slot sl): rhs and cross-color gathers
+                          P.fflag + k, P.s_ns);
+    // dynamic operands of walk step i in slot sl: rhs and cross-color gathers
     auto gather = [&](int i, int sl, double *x, double &rhs) {
-      const int l = it.fwd ? i : b_s - 1 - i;
-      const int row = blk0 + l * 32 + lane;
-      rhs = __ldcg(rhs_v + row);
+      const int l = fwd ? i : b_s - 1 - i;
+      rhs = __ldcg(rhs_v + blk0 + l * 32 + lane);
       const int *sc = (const int *)(wb + (size_t)sl * SB + (size_t)LC * 256);
       const int len = slen[sl];
 #pragma unroll
       for (int u = 0; u < KG; ++u) {
-        double v = 0.0;
-        if (u < len) {
-          const int c = sc[u * 32 + lane];
-          if ((unsigned)(c - blk0) >= uspan) v = __ldcg(out + c);
-        }
-        x[u] = v;
+        const int c = u < len ? sc[u * 32 + lane] : blk0;
+        x[u] = (unsigned)(c - blk0) >= uspan ? __ldcg(out + c) : 0.0;
       }
     };
-    wait_group<D - 1>();
-    __syncwarp();
-    double rhs_a = 0.0, rhs_b = 0.0;
-    gather(0, cslot, xa, rhs_a);
-    for (int i = 0; i < b_s; ++i) {
-      const int nslot = cslot + 1 == D ? 0 : cslot + 1;
-      if (i + 1 < b_s) {
-        wait_group<D - 2>();
-        __syncwarp();
-        gather(i + 1, nslot, xb, rhs_b);
-      }
-      const int l = it.fwd ? i : b_s - 1 - i;
+    // walk step i from slot sl with its gathers x (x_next: the next step's,
+    // issued before this step's chain)
+    auto step = [&](int i, int sl, const double *x, double rhs) {
+      const int l = fwd ? i : b_s - 1 - i;
       const int row = blk0 + l * 32 + lane;
-      const unsigned char *sl = wb + (size_t)cslot * SB;
-      const double *sv = (const double *)sl;
-      const int *sc = (const int *)(sl + (size_t)LC * 256);
-      const double idg = ((const double *)(sl + (size_t)LC * 384))[lane];
-      const int len = slen[cslot];
-      double y = rhs_a;
+      const unsigned char *sp = wb + (size_t)sl * SB;
+      const double *sv = (const double *)sp;
+      const int *sc = (const int *)(sp + (size_t)LC * 256);
+      const double idg = ((const double *)(sp + (size_t)LC * 384))[lane];
+      const int len = slen[sl];
+      double y = rhs;
       auto update = [&](int cc, double vv, double xcross) {
         const unsigned rel = (unsigned)(cc - blk0);
         const bool inblk = rel < uspan;
         unsigned lp = rel >> 5;
         lp = lp < (unsigned)b_s ? lp : 0u;
-        const double ysv = ys[(it.fwd ? (int)lp : b_s - 1 - (int)lp) * 32 + lane];
+        const double ysv = ys[(fwd ? (int)lp : b_s - 1 - (int)lp) * 32 + lane];
         const double xin = cc == row ? y : ysv;
         y = __dsub_rn(y, __dmul_rn(vv, inblk ? xin : xcross));
       };
 #pragma unroll
       for (int u = 0; u < KG; ++u)
-        if (u < len) update(sc[u * 32 + lane], sv[u * 32 + lane], xa[u]);
+        if (u < len) update(sc[u * 32 + lane], sv[u * 32 + lane], x[u]);
       for (int t = KG; t < len; ++t) {
         const int cc = sc[t * 32 + lane];
         const double xc = (unsigned)(cc - blk0) < uspan ? 0.0 : __ldcg(out + cc);
@@ -211,15 +200,42 @@ __device__ __forceinline__ void run(const persist::Params &P, unsigned char *sme
       y = __dmul_rn(y, idg);
       ys[i * 32 + lane] = y;
       out[row] = y;
-      __syncwarp();   // every lane is done with slot cslot (and ys[i] is visible)
-      issue();        // refill it with the step D ahead
-      cslot = nslot;
-#pragma unroll
-      for (int u = 0; u < KG; ++u) xa[u] = xb[u];
-      rhs_a = rhs_b;
+    };
+    wait_group<D - 1>();
+    __syncwarp();
+    double ra = 0.0, rb = 0.0;
+    gather(0, cslot, xa, ra);
+    // two steps per trip, register buffers used ping-pong (no copies)
+    int i = 0;
+    for (; i + 1 < b_s; i += 2) {
+      const int s1 = cslot + 1 == D ? 0 : cslot + 1;
+      wait_group<D - 2>();
+      __syncwarp();
+      gather(i + 1, s1, xb, rb);
+      step(i, cslot, xa, ra);
+      __syncwarp();
+      issue();
+      cslot = s1;
+      const int s2 = cslot + 1 == D ? 0 : cslot + 1;
+      if (i + 2 < b_s) {
+        wait_group<D - 2>();
+        __syncwarp();
+        gather(i + 2, s2, xa, ra);
+      }
+      step(i + 1, cslot, xb, rb);
+      __syncwarp();
+      issue();
+      cslot = s2;
+    }
+    if (i < b_s) {   // odd b_s: the last step's gathers are in xa
+      const int s1 = cslot + 1 == D ? 0 : cslot + 1;
+      step(i, cslot, xa, ra);
+      __syncwarp();
+      issue();
+      cslot = s1;
     }
     __syncwarp();
-    if (lane == 0) persist::st_release((it.fwd ? P.fflag : P.bflag) + k, epoch);
+    if (lane == 0) persist::st_release((fwd ? P.fflag : P.bflag) + k, epoch);
   }
   wait_group<0>();
 }
