@@ -38,7 +38,6 @@ using tb::fail;
 #include "sweep_lean.cuh"
 #include "spmv_tma.cuh"
 #include "persist.cuh"
-#include "sweep_stream.cuh"
 
 #define CU(call)                                                          \
   do {                                                                    \
@@ -779,16 +778,6 @@ __global__ void __launch_bounds__(persist::kThreads, TB_PRE_MINB)
                                    lens);
 }
 
-// Streamed preconditioner application (sweep_stream.cuh): the dataflow
-// item sequence with every warp's static operands cp.async-streamed D steps
-// ahead into shared memory and the dynamic ones gathered a step ahead.
-template <int KG, int D>
-__global__ void __launch_bounds__(256)
-    precond_stream(const __grid_constant__ persist::Params P) {
-  extern __shared__ __align__(16) unsigned char ssm[];
-  sweep_stream::run<KG, D>(P, ssm);
-}
-
 // ------------------------------------------------------------ helpers
 inline unsigned grid_for(long long n, int per_block = kBlock) {
   long long g = (n + per_block - 1) / per_block;
@@ -1023,9 +1012,7 @@ struct tb_plan {
   int spmv_S = 0, spmv_cap = 0, spmv_D = 0, spmv_grid = 0;
   // precond-only dataflow kernel (0 = use pcg_persistent mode 0)
   int pre_grid = 0;
-  // streamed dataflow precond (sweep_stream.cuh; 0 = not configured)
-  int stream_grid = 0, stream_block = 0, stream_kg = 0, stream_D = 0, stream_lc = 0;
-  size_t stream_smem = 0;
+
   // tb_pcg as a host-polled kernel sequence with the TMA SpMV and one
   // persistent dataflow precond launch per iteration (large systems)
   bool split_pcg = false;
@@ -1493,57 +1480,6 @@ PersistFn persist_fn(int kc, bool flow) {
   }
 }
 
-using StreamFn = void (*)(persist::Params);
-StreamFn stream_fn(int kg, int D) {
-#define TB_SF(K)                                                                       \
-  if (kg == K) return D == 2 ? precond_stream<K, 2> : D == 3 ? precond_stream<K, 3> \
-                                                             : precond_stream<K, 4>;
-  TB_SF(4) TB_SF(8)
-#undef TB_SF
-  return D == 2 ? precond_stream<16, 2> : D == 3 ? precond_stream<16, 3> : precond_stream<16, 4>;
-}
-
-// Size the streamed precond: KG = gathers held per step (>= the longest
-// slice up to 16), ring depth D and warps per CTA chosen for the most warps
-// per SM (shared memory bound), preferring D = 4 when >= 12 warps fit.
-int configure_stream(tb_plan *pl, long long lmax) {
-  pl->stream_grid = 0;
-  if (env_int("TB_STREAM", 1) == 0 || pl->n_lvl1_flow == 0) return TB_OK;
-  const int lc = (int)(lmax < 1 ? 1 : lmax);
-  const int kg = lc <= 4 ? 4 : (lc <= 8 ? 8 : 16);
-  int optin = 0;
-  CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
-  int best_w = 0, best_D = 0, best_wpc = 0, best_ps = 0;
-  for (int D : {4, 3, 2}) {
-    for (int wpc : {8, 4}) {
-      const size_t sm = (size_t)wpc * sweep_stream::warp_bytes(lc, D, (int)pl->b_s);
-      if (sm > (size_t)optin) continue;
-      StreamFn fn = stream_fn(kg, D);
-      CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-      int ps = 0;
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, wpc * 32, sm));
-      if (ps * wpc > best_w) {
-        best_w = ps * wpc;
-        best_wpc = wpc;
-        best_ps = ps;
-      }
-    }
-    if (best_w > 0 && (best_w >= 12 || D == 2)) {
-      best_D = D;
-      break;
-    }
-    best_w = 0;
-  }
-  if (best_D == 0 || best_ps < 1) return TB_OK;
-  pl->stream_kg = kg;
-  pl->stream_D = best_D;
-  pl->stream_lc = lc;
-  pl->stream_block = best_wpc * 32;
-  pl->stream_smem = (size_t)best_wpc * sweep_stream::warp_bytes(lc, best_D, (int)pl->b_s);
-  pl->stream_grid = best_ps * pl->num_sms;
-  return TB_OK;
-}
-
 using PreFn = void (*)(persist::Params);
 PreFn pre_fn(int kc) {
   switch (kc) {
@@ -1672,7 +1608,6 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
         if (ps > cap) ps = cap;
         pl->pre_grid = ps > 0 ? ps * pl->num_sms : 0;
       }
-      if ((rc = configure_stream(pl, lmax))) return rc;
     }
   }
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
@@ -1768,23 +1703,6 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.state = pl->st;
   P.watchdog = 4000000000LL;  // ~2 s at 1.9 GHz per barrier wait
   void *args[] = {&P};
-  if (mode == 0 && P.n_lvl1 > 0 && pl->stream_grid > 0) {
-    // streamed precond; in a graph the epoch comes from device memory (see
-    // below).  Launched cooperatively outside graphs so the grid is resident.
-    P.s_LC = pl->stream_lc;
-    StreamFn fn = stream_fn(pl->stream_kg, pl->stream_D);
-    if (pl->in_graph) {
-      P.epoch_dev = pl->epoch_dev;
-      fn<<<pl->stream_grid, pl->stream_block, pl->stream_smem, s>>>(P);
-      if (!pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
-    } else {
-      void *a2[] = {&P};
-      CU(cudaLaunchCooperativeKernel((const void *)fn, dim3(pl->stream_grid),
-                                     dim3(pl->stream_block), a2, pl->stream_smem, s));
-    }
-    CU(cudaGetLastError());
-    return TB_OK;
-  }
   if (mode == 0 && P.n_lvl1 > 0 && pl->in_graph) {
     // captured into the split PCG graph: the epoch comes from device memory
     // (bumped by a 1-thread kernel after each application) and the launch is

@@ -79,7 +79,6 @@ struct Params {
   int n_lvl1;             // 0 = use the barrier-separated color phases
   unsigned epoch;         // epoch of the first preconditioner application
   const unsigned *epoch_dev;  // mode 0 in a CUDA graph: epoch read from here (else null)
-  int s_LC;               // streamed precond (sweep_stream.cuh): slot capacity in slots
 };
 
 __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
