@@ -250,7 +250,7 @@ typedef struct {
     int32_t precond_kind;       /* TB_PRECOND_* */
     int32_t spmv_format;        /* TB_SPMV_* */
     int64_t n;                  /* system size (n_pad for HBMC) */
-    int64_t n_real;             /* real unknowns (reporting only) */
+    int64_t n_real;             /* real unknowns (see real_pos) */
     const double *inv_d;        /* [n] */
     /* HBMC */
     int64_t w, b_s, n_c;
@@ -264,6 +264,11 @@ typedef struct {
     tb_csr_host A_csr;
     /* TB_PLAN_* flags (ABI 2) */
     int64_t flags;
+    /* ABI 3: the n_real sorted positions of the real unknowns (HbmcLayout
+     * real_positions, src/ordering.py:263) when n_real < n, else NULL.  The
+     * solver's dot products run over exactly these rows, in this order
+     * (src/solver.py:150-153), so dummy rows never change a reduction. */
+    const int64_t *real_pos;
 } tb_plan_desc;
 
 /* The plan is one rank of a row-partitioned system (partition.py): columns

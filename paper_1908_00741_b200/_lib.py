@@ -27,7 +27,7 @@ TB_SPMV_SELL = 0
 TB_SPMV_CSR = 1
 TB_SPMV_NONE = 2
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 TB_PLAN_PARTITIONED = 1
 
 i64 = C.c_int64
@@ -59,7 +59,8 @@ class TbPlanDesc(C.Structure):
                 ("L_sell", TbSellHost), ("U_sell", TbSellHost),
                 ("L_csr", TbCsrHost), ("U_csr", TbCsrHost),
                 ("fwd_sched", TbSchedHost), ("bwd_sched", TbSchedHost),
-                ("A_sell", TbSellHost), ("A_csr", TbCsrHost), ("flags", i64)]
+                ("A_sell", TbSellHost), ("A_csr", TbCsrHost), ("flags", i64),
+                ("real_pos", vp)]
 
 
 TB_MAX_PEERS = 16

@@ -40,7 +40,7 @@ using tb::fail;
 
 extern "C" const char *tb_last_error(void) { return tb::g_err.c_str(); }
 
-extern "C" int tb_abi_version(void) { return 2; }
+extern "C" int tb_abi_version(void) { return 3; }
 
 #define TB_TRY_BEGIN try {
 #define TB_TRY_END                                              \

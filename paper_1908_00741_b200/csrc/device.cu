@@ -181,6 +181,52 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// ------------------------------------------------------------ real-row loops
+// Plans with dummy rows (HBMC padding) pass rix = the sorted real positions
+// (HbmcLayout.real_positions): every CG vector kernel then walks rho in
+// [0, n_real) with element i = rix[rho], in exactly the thread / unit
+// assignment of its plain loop over a system of n_real rows (PAIRS: a unit is
+// two consecutive rho, like TB_PAIRS4's element pair).  So every dot product
+// -- and every x, r, p update -- is the one the same kernels compute for the
+// system without dummies: the reduction tree depends only on the sequence of
+// real entries (src/solver.py:150-153 reduces over real positions only),
+// and HBMC with w = 1 reproduces BMC bitwise (T/test_solver.py:137-145).
+// Dummy entries of x, r, p are never touched (they stay 0: b is 0 there).
+template <bool PAIRS, class F>
+__device__ __forceinline__ void rloop(long long n, const int *__restrict__ rix, F f) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long nu = PAIRS ? n / 2 : n;
+  long long u0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  auto unit = [&](long long u) {
+    if (PAIRS) {
+      f((long long)__ldg(rix + 2 * u));
+      f((long long)__ldg(rix + 2 * u + 1));
+    } else {
+      f((long long)__ldg(rix + u));
+    }
+  };
+  for (; u0 + 3 * stride < nu; u0 += 4 * stride) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) unit(u0 + q * stride);
+  }
+  for (; u0 < nu; u0 += stride) unit(u0);
+}
+
+// p.Ap epilogue shared by the SpMV kernels: alpha = rz / p.Ap, or the CG
+// breakdown (src/solver.py:174-177).
+__device__ __forceinline__ void pap_fin(PcgState *st, double pap) {
+  const long long j = st->iter + 1;
+  st->pap = pap;
+  if (pap <= 0.0) {
+    st->status = TB_ECG_BREAKDOWN;
+    st->bd_iter = j;
+    st->bd_val = pap;
+    stop_loop(st);
+    return;
+  }
+  st->alpha = st->rz / pap;
+}
+
 // ------------------------------------------------------------ SpMV
 // K/numba_backend.py:26-37: out = 0; out += v * x[col] per slot in stored
 // order.  Optional fused epilogue: pap = p . (A p) and alpha = rz / pap.
@@ -190,19 +236,18 @@ __global__ void __launch_bounds__(kBlock)
               const int *__restrict__ slice_len, const int *__restrict__ col,
               const double *__restrict__ val, int w,
               const double *__restrict__ x, double *__restrict__ out,
-              double *partials, PcgState *st) {
+              double *partials, PcgState *st, const int *rix = nullptr) {
   if (DOT && st->done) return;
   double part = 0.0;
   constexpr int CH = 8;  // slots whose loads / gathers are in flight together
-  for (long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x; row < n;
-       row += (long long)gridDim.x * blockDim.x) {
+  auto row_fn = [&](long long row) {
     if (PAIRED) {
       const long long s = row / w;
       const double acc = persist::sell_row_paired<4>(val, col, (int)slice_ptr[s], slice_len[s],
                                                      w, (int)(row - s * w), x);
       out[row] = acc;
       if (DOT) part += __ldcg(x + row) * acc;
-      continue;
+      return;
     }
     const long long s = row / w;
     const int j = (int)(row - s * w);
@@ -229,20 +274,15 @@ __global__ void __launch_bounds__(kBlock)
     }
     out[row] = acc;
     if (DOT) part += xr * acc;
+  };
+  if (rix) {
+    rloop<false>(n, rix, row_fn);
+  } else {
+    for (long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+         row += (long long)gridDim.x * blockDim.x)
+      row_fn(row);
   }
-  if (DOT)
-    grid_reduce(part, partials, &st->counter[0], [st](double pap) {
-      const long long j = st->iter + 1;
-      st->pap = pap;
-      if (pap <= 0.0) {  // src/solver.py:176-177
-        st->status = TB_ECG_BREAKDOWN;
-        st->bd_iter = j;
-        st->bd_val = pap;
-        stop_loop(st);
-        return;
-      }
-      st->alpha = st->rz / pap;
-    });
+  if (DOT) grid_reduce(part, partials, &st->counter[0], [st](double pap) { pap_fin(st, pap); });
 }
 
 // K/numba_backend.py:16-23 spmv_csr (thread per row).
@@ -251,30 +291,35 @@ __global__ void __launch_bounds__(kBlock)
     spmv_csr(long long n, const long long *__restrict__ rp,
              const int *__restrict__ col, const double *__restrict__ val,
              const double *__restrict__ x, double *__restrict__ out,
-             double *partials, PcgState *st) {
+             double *partials, PcgState *st, const int *rix = nullptr) {
   if (DOT && st->done) return;
   double part = 0.0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
+  auto row_fn = [&](long long i) {
     double acc = 0.0;
     for (long long p = rp[i]; p < rp[i + 1]; ++p)
       acc = __dadd_rn(acc, __dmul_rn(val[p], x[col[p]]));
     out[i] = acc;
     if (DOT) part += x[i] * acc;
+  };
+  if (rix) {
+    rloop<false>(n, rix, row_fn);
+  } else {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+      row_fn(i);
   }
-  if (DOT)
-    grid_reduce(part, partials, &st->counter[0], [st](double pap) {
-      const long long j = st->iter + 1;
-      st->pap = pap;
-      if (pap <= 0.0) {
-        st->status = TB_ECG_BREAKDOWN;
-        st->bd_iter = j;
-        st->bd_val = pap;
-        stop_loop(st);
-        return;
-      }
-      st->alpha = st->rz / pap;
-    });
+  if (DOT) grid_reduce(part, partials, &st->counter[0], [st](double pap) { pap_fin(st, pap); });
+}
+
+// p . Ap over the real rows after a plain SpMV (plans with dummy rows whose
+// SpMV is the TMA-staged kernel, which has no real-row loop).
+__global__ void __launch_bounds__(kBlock)
+    cg_dot_pap(long long n, const double *__restrict__ p, const double *__restrict__ ap,
+               const int *__restrict__ rix, double *partials, PcgState *st) {
+  if (st->done) return;
+  double part = 0.0;
+  rloop<false>(n, rix, [&](long long i) { part += __ldcg(p + i) * __ldcg(ap + i); });
+  grid_reduce(part, partials, &st->counter[0], [st](double pap) { pap_fin(st, pap); });
 }
 
 // TMA-staged SpMV (spmv_tma.cuh) with the fused p . Ap and alpha epilogue
@@ -286,18 +331,7 @@ __global__ void __launch_bounds__(spmv_tma::kThreads, 2)
   spmv_tma::init_bars(p, smem);
   unsigned phase = 0;
   const double part = spmv_tma::run<true>(p, smem, phase);
-  grid_reduce(part, partials, &st->counter[0], [st](double pap) {
-    const long long j = st->iter + 1;
-    st->pap = pap;
-    if (pap <= 0.0) {  // src/solver.py:176-177
-      st->status = TB_ECG_BREAKDOWN;
-      st->bd_iter = j;
-      st->bd_val = pap;
-      stop_loop(st);
-      return;
-    }
-    st->alpha = st->rz / pap;
-  });
+  grid_reduce(part, partials, &st->counter[0], [st](double pap) { pap_fin(st, pap); });
 }
 
 // ------------------------------------------------------------ CG vectors
@@ -305,15 +339,16 @@ __global__ void __launch_bounds__(spmv_tma::kThreads, 2)
 __global__ void __launch_bounds__(kBlock)
     cg_init(long long n, const double *__restrict__ b, double *__restrict__ x,
             double *__restrict__ r, double *partials, PcgState *st,
-            double *hist) {
+            double *hist, long long n_red = 0, const int *rix = nullptr) {
   double part = 0.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const double bi = b[i];
     x[i] = 0.0;
     r[i] = bi;
-    part += bi * bi;
+    if (!rix) part += bi * bi;
   }
+  if (rix) rloop<false>(n_red, rix, [&](long long i) { part += b[i] * b[i]; });
   grid_reduce(part, partials, &st->counter[1], [st, hist](double bb) {
     st->bnorm = sqrt(bb);
     st->iter = 0;
@@ -370,11 +405,18 @@ __global__ void __launch_bounds__(kBlock)
     cg_update_xr(long long n, const double *__restrict__ p,
                  const double *__restrict__ ap, double *__restrict__ x,
                  double *__restrict__ r, double *partials, PcgState *st,
-                 double *hist) {
+                 double *hist, const int *rix = nullptr) {
   if (st->done) return;
   const double alpha = st->alpha;
   double part = 0.0;
-  if (PAIRS) {   // 16-byte accesses (n even)
+  if (rix) {     // real rows only, same association (n = real rows)
+    rloop<PAIRS>(n, rix, [&](long long i) {
+      if (!FOLDX) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+      const double ri = __dsub_rn(r[i], __dmul_rn(alpha, ap[i]));
+      r[i] = ri;
+      part += ri * ri;
+    });
+  } else if (PAIRS) {   // 16-byte accesses (n even)
     TB_PAIRS4({
       if (!FOLDX) {
         const double2 xo = *(const double2 *)(x + i), po = *(const double2 *)(p + i);
@@ -524,20 +566,30 @@ template <bool FOLDX = false>
 __global__ void __launch_bounds__(kBlock)
     cg_rz_p_coop(long long n, const double *__restrict__ r, const double *__restrict__ z,
                  double *__restrict__ p, double *partials, unsigned *bar, PcgState *st,
-                 double *__restrict__ x, unsigned *epoch_bump) {
+                 double *__restrict__ x, unsigned *epoch_bump, const int *rix) {
   __shared__ double sh[33];
   if (st->done) return;
   const double rz_old = st->rz;
   const double alpha = st->alpha;   // this iteration's, for the deferred x update
   double part = 0.0;
-  TB_PAIRS4({
-    const double2 zi = *(const double2 *)(z + i), ri = *(const double2 *)(r + i);
-    part += ri.x * zi.x;
-    part += ri.y * zi.y;
-  })
+  if (rix) {
+    rloop<true>(n, rix, [&](long long i) { part += r[i] * z[i]; });
+  } else {
+    TB_PAIRS4({
+      const double2 zi = *(const double2 *)(z + i), ri = *(const double2 *)(r + i);
+      part += ri.x * zi.x;
+      part += ri.y * zi.y;
+    })
+  }
   const double rzn = coop_sum(part, partials, bar, sh);
   const double beta = rzn / rz_old;
-  TB_PAIRS4({
+  if (rix) {
+    rloop<true>(n, rix, [&](long long i) {
+      const double po = p[i];
+      if (FOLDX) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, po));
+      p[i] = __dadd_rn(z[i], __dmul_rn(beta, po));
+    });
+  } else TB_PAIRS4({
     const double2 zi = *(const double2 *)(z + i), po = *(const double2 *)(p + i);
     if (FOLDX) {   // x += alpha p with the p this iteration's x/r pass used
       const double2 xo = *(const double2 *)(x + i);
@@ -562,9 +614,13 @@ __global__ void __launch_bounds__(kBlock)
 // p update never ran: every exit happens at the residual check or before).
 __global__ void __launch_bounds__(kBlock)
     cg_x_final(long long n, const double *__restrict__ p, double *__restrict__ x,
-               const PcgState *st) {
+               const PcgState *st, const int *rix) {
   if (st->status != TB_OK || st->iter < 1) return;
   const double alpha = st->alpha;
+  if (rix) {
+    rloop<false>(n, rix, [&](long long i) { x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i])); });
+    return;
+  }
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
@@ -576,10 +632,16 @@ template <bool FIRST, bool PAIRS = false>
 __global__ void __launch_bounds__(kBlock)
     cg_rz(long long n, const double *__restrict__ r,
           const double *__restrict__ z, double *__restrict__ p,
-          double *partials, PcgState *st) {
+          double *partials, PcgState *st, const int *rix = nullptr) {
   if (st->done) return;
   double part = 0.0;
-  if (PAIRS) {
+  if (rix) {
+    rloop<PAIRS>(n, rix, [&](long long i) {
+      const double zi = z[i];
+      part += r[i] * zi;
+      if (FIRST) p[i] = zi;
+    });
+  } else if (PAIRS) {
     TB_PAIRS4({
       const double2 zi = *(const double2 *)(z + i), ri = *(const double2 *)(r + i);
       part += ri.x * zi.x;
@@ -607,10 +669,12 @@ __global__ void __launch_bounds__(kBlock)
 template <bool PAIRS = false>
 __global__ void __launch_bounds__(kBlock)
     cg_update_p(long long n, const double *__restrict__ z,
-                double *__restrict__ p, const PcgState *st) {
+                double *__restrict__ p, const PcgState *st, const int *rix = nullptr) {
   if (st->done) return;
   const double beta = st->beta;
-  if (PAIRS) {
+  if (rix) {
+    rloop<PAIRS>(n, rix, [&](long long i) { p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i])); });
+  } else if (PAIRS) {
     TB_PAIRS4({
       const double2 zi = *(const double2 *)(z + i), po = *(const double2 *)(p + i);
       double2 pn;
@@ -1019,6 +1083,10 @@ struct tb_plan {
   int vec_pt = 16;             // elements per thread of the CG vector kernels (grid size)
   int xr_grid = 0;             // spmv_tma_xr cooperative grid (0 = separate x/r pass)
   int rzp_grid = 0;            // cg_rz_p_coop cooperative grid (0 = cg_rz + cg_update_p)
+  // plans with dummy rows: the real positions (int32, sorted) the CG vector
+  // kernels walk (see rloop); n_red = their count (= n without dummies)
+  int *rix = nullptr;
+  long long n_red = 0;
   bool in_graph = false;       // capturing the split graph: precond epochs from epoch_dev
   bool defer_bump = false;     // the iteration's cg_rz_p_coop bumps the epoch instead
   bool g_split = false;        // the instantiated graph is the split variant
@@ -1175,10 +1243,17 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
   if (n <= 0) return TB_OK;
   if (pl->spmv_format == TB_SPMV_NONE)
     return fail(TB_EINVAL, "plan has no matrix A (preconditioner-only plan)");
+  const long long nr = pl->n_red;
   if (pl->spmv_format == TB_SPMV_SELL && pl->spmv_S > 0) {
     spmv_tma::Params P;
     spmv_params(pl, x, out, P);
-    if (dot)
+    if (dot && pl->rix) {   // real-row p.Ap after the plain TMA SpMV
+      spmv_tma::spmv_kernel<<<pl->spmv_grid, spmv_tma::kThreads,
+                              spmv_tma::smem_bytes(P.cap, P.D), s>>>(P);
+      ++*nl;
+      cg_dot_pap<<<reduce_grid(nr, 1), kBlock, 0, s>>>(nr, x, out, pl->rix, pl->partials,
+                                                        pl->st);
+    } else if (dot)
       spmv_tma_dot<<<pl->spmv_grid, spmv_tma::kThreads, spmv_tma::smem_bytes(P.cap, P.D), s>>>(
           P, pl->partials, pl->st);
     else
@@ -1187,18 +1262,18 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
   } else if (pl->spmv_format == TB_SPMV_SELL) {
     if (dot)
       (pl->A.paired ? spmv_sell<true, true> : spmv_sell<true, false>)
-          <<<reduce_grid(n, 1), kBlock, 0, s>>>(n, pl->A.slice_ptr, pl->A.slice_len,
-                                                pl->A.col, pl->A.val, (int)pl->A.width, x,
-                                                out, pl->partials, pl->st);
+          <<<reduce_grid(nr, 1), kBlock, 0, s>>>(nr, pl->A.slice_ptr, pl->A.slice_len,
+                                                 pl->A.col, pl->A.val, (int)pl->A.width, x,
+                                                 out, pl->partials, pl->st, pl->rix);
     else
       (pl->A.paired ? spmv_sell<false, true> : spmv_sell<false, false>)
           <<<grid_for(n), kBlock, 0, s>>>(n, pl->A.slice_ptr, pl->A.slice_len, pl->A.col,
                                           pl->A.val, (int)pl->A.width, x, out, nullptr,
-                                          nullptr);
+                                          nullptr, nullptr);
   } else {
     if (dot)
-      spmv_csr<true><<<reduce_grid(n), kBlock, 0, s>>>(
-          n, pl->Ac.rp, pl->Ac.col, pl->Ac.val, x, out, pl->partials, pl->st);
+      spmv_csr<true><<<reduce_grid(nr), kBlock, 0, s>>>(
+          nr, pl->Ac.rp, pl->Ac.col, pl->Ac.val, x, out, pl->partials, pl->st, pl->rix);
     else
       spmv_csr<false><<<grid_for(n), kBlock, 0, s>>>(
           n, pl->Ac.rp, pl->Ac.col, pl->Ac.val, x, out, nullptr, nullptr);
@@ -1215,14 +1290,15 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
 // x += alpha p folded into the p update (TB_FOLD_X=0 disables): only with
 // the cooperative r.z + p kernel, which then owns that update.
 bool fold_x(const tb_plan *pl) {
-  return (pl->n % 2) == 0 && env_int("TB_VEC_PAIRS", 1) && pl->rzp_grid > 0 && pl->bar &&
+  return (pl->n_red % 2) == 0 && env_int("TB_VEC_PAIRS", 1) && pl->rzp_grid > 0 && pl->bar &&
          env_int("TB_FOLD_X", 1);
 }
 
 // The deferred x update of the last iteration (FOLDX solves).
 int launch_x_final(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   if (!fold_x(pl)) return TB_OK;
-  cg_x_final<<<reduce_grid(pl->n, pl->vec_pt), kBlock, 0, s>>>(pl->n, pl->p, x, pl->st);
+  cg_x_final<<<reduce_grid(pl->n_red, pl->vec_pt), kBlock, 0, s>>>(pl->n_red, pl->p, x, pl->st,
+                                                                   pl->rix);
   ++*nl;
   CU(cudaGetLastError());
   return TB_OK;
@@ -1253,10 +1329,10 @@ int debug_sync(tb_plan *pl, cudaStream_t s, const char *stage) {
 }
 
 int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
-  const long long n = pl->n;
+  const long long n = pl->n_red;   // the vector kernels' rows (real rows, via pl->rix)
   const unsigned rg = reduce_grid(n, pl->vec_pt);
   int rc;
-  if (pl->split_pcg && pl->xr_grid > 0) {
+  if (pl->split_pcg && pl->xr_grid > 0 && !pl->rix) {
     spmv_tma::Params P;
     spmv_params(pl, pl->p, pl->ap, P);
     double *xx = x, *rr = pl->r, *pp = pl->partials;
@@ -1275,7 +1351,8 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
     const bool pairs = (n % 2) == 0 && env_int("TB_VEC_PAIRS", 1);
     const bool fold = fold_x(pl);
     (fold ? cg_update_xr<true, true> : pairs ? cg_update_xr<true> : cg_update_xr<false>)
-        <<<rg, kBlock, 0, s>>>(n, pl->p, pl->ap, x, pl->r, pl->partials, pl->st, pl->hist);
+        <<<rg, kBlock, 0, s>>>(n, pl->p, pl->ap, x, pl->r, pl->partials, pl->st, pl->hist,
+                               pl->rix);
     ++*nl;
     if ((rc = debug_sync(pl, s, "cg_update_xr"))) return rc;
   }
@@ -1295,18 +1372,19 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
     unsigned *bb = pl->bar;
     PcgState *ss = pl->st;
     unsigned *eb = pl->defer_bump ? pl->epoch_dev : nullptr;
+    const int *rx = pl->rix;
     pl->defer_bump = false;
-    void *args[] = {&nn, &rr, &zz, &pp, &pa, &bb, &ss, &xx, &eb};
+    void *args[] = {&nn, &rr, &zz, &pp, &pa, &bb, &ss, &xx, &eb, &rx};
     CU(cudaLaunchCooperativeKernel(fold_x(pl) ? (const void *)cg_rz_p_coop<true>
                                               : (const void *)cg_rz_p_coop<false>,
                                    dim3(pl->rzp_grid), dim3(kBlock), args, 0, s));
     --*nl;   // one launch instead of two
   } else {
     (pairs2 ? cg_rz<false, true> : cg_rz<false, false>)<<<rg, kBlock, 0, s>>>(
-        n, pl->r, pl->z, pl->p, pl->partials, pl->st);
+        n, pl->r, pl->z, pl->p, pl->partials, pl->st, pl->rix);
     if ((rc = debug_sync(pl, s, "cg_rz"))) return rc;
     (pairs2 ? cg_update_p<true> : cg_update_p<false>)<<<reduce_grid(n, pl->vec_pt), kBlock, 0, s>>>(
-        n, pl->z, pl->p, pl->st);
+        n, pl->z, pl->p, pl->st, pl->rix);
   }
   *nl += 2;
   if ((rc = debug_sync(pl, s, "cg_update_p"))) return rc;
@@ -1316,13 +1394,13 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
 
 int launch_prologue(tb_plan *pl, const double *b, double *x, cudaStream_t s,
                     long long *nl) {
-  const long long n = pl->n;
-  const unsigned rg = reduce_grid(n);
+  const long long n = pl->n, nr = pl->n_red;
+  const unsigned rg = reduce_grid(nr);
   int rc;
-  cg_init<<<rg, kBlock, 0, s>>>(n, b, x, pl->r, pl->partials, pl->st, pl->hist);
+  cg_init<<<rg, kBlock, 0, s>>>(n, b, x, pl->r, pl->partials, pl->st, pl->hist, nr, pl->rix);
   ++*nl;
   if ((rc = launch_precond_step(pl, s, nl))) return rc;
-  cg_rz<true><<<rg, kBlock, 0, s>>>(n, pl->r, pl->z, pl->p, pl->partials, pl->st);
+  cg_rz<true><<<rg, kBlock, 0, s>>>(nr, pl->r, pl->z, pl->p, pl->partials, pl->st, pl->rix);
   ++*nl;
   CU(cudaGetLastError());
   return TB_OK;
@@ -1611,14 +1689,6 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
     }
   }
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
-  if (env_int("TB_RZP_FUSE", 1)) {   // fused r.z + p update for the kernel-sequence paths
-    int ps = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cg_rz_p_coop<true>, kBlock, 0));
-    const long long want = ((pl->n + 1) / 2 + kBlock * 8 - 1) / (kBlock * 8);  // ~16 elements/thread
-    long long g = (long long)ps * pl->num_sms;
-    if (want < g) g = want;
-    pl->rzp_grid = g > 0 ? (int)g : 0;
-  }
   // Without the dataflow schedule a small system runs faster as per-phase
   // kernels in a CUDA graph (config 1: ICCG 2.01 vs 2.44 ms, precond 36 vs
   // 61 us); large barrier-mode systems keep the single launch (config 4:
@@ -1925,6 +1995,37 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
   for (double *v : {pl->r, pl->y, pl->z, pl->p, pl->ap})
     if (cudaMemset(v, 0xff, sizeof(double) * (size_t)nv) != cudaSuccess)
       return bail(fail(TB_ECUDA, "plan_create: memset failed"));
+  // real positions (plans with dummy rows): the reduction index of the CG
+  // vector kernels; sorted, in range
+  pl->n_red = d->n;
+  if (d->real_pos && d->n_real > 0 && d->n_real < d->n) {
+    std::vector<int> rp((size_t)d->n_real);
+    for (long long i = 0; i < d->n_real; ++i) {
+      const long long v = d->real_pos[i];
+      if (v < 0 || v >= d->n || (i > 0 && v <= d->real_pos[i - 1]))
+        return bail(fail(TB_EINVAL, "plan_create: real_pos must be sorted positions < n"));
+      rp[(size_t)i] = (int)v;
+    }
+    if ((rc = upload(&pl->rix, rp.data(), d->n_real))) return bail(rc);
+    pl->n_red = d->n_real;
+    // the single-launch persistent PCG reduces over all rows: plans with
+    // dummies solve through the kernel-sequence paths
+    pl->persist_pcg_ok = false;
+  }
+  if (!pl->bar) {   // grid barrier of the cooperative vector kernels
+    if (cudaMalloc((void **)&pl->bar, 2 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(pl->bar, 0, 2 * sizeof(unsigned)) != cudaSuccess)
+      return bail(fail(TB_ECUDA, "plan_create: barrier allocation failed"));
+  }
+  if (env_int("TB_RZP_FUSE", 1)) {   // fused r.z + p update for the kernel-sequence paths
+    int ps = 0, nsm = 148;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cg_rz_p_coop<true>, kBlock, 0));
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
+    const long long want = ((pl->n_red + 1) / 2 + kBlock * 8 - 1) / (kBlock * 8);  // ~16 elements/thread
+    long long g = (long long)ps * nsm;
+    if (want < g) g = want;
+    pl->rzp_grid = g > 0 ? (int)g : 0;
+  }
   if (cudaMalloc((void **)&pl->st, sizeof(PcgState)) != cudaSuccess ||
       cudaMemset(pl->st, 0, sizeof(PcgState)) != cudaSuccess)
     return bail(fail(TB_ECUDA, "plan_create: state allocation failed"));
@@ -1951,6 +2052,7 @@ extern "C" int tb_plan_destroy(tb_plan *pl) {
   cudaFree(pl->inv_d);
   cudaFree(pl->vec_pool);
   cudaFree(pl->partials);
+  cudaFree(pl->rix);
   cudaFree(pl->st);
   cudaFree(pl->hist);
   cudaFree(pl->color_lvl1_dev);

@@ -214,7 +214,7 @@ class DevicePlan:
     def __init__(self, *, kind, n, n_real, inv_d, spmv_format,
                  w=0, b_s=0, color_lvl1_ranges=None, L_sell=None, U_sell=None,
                  L_csr=None, U_csr=None, fwd_sched=None, bwd_sched=None,
-                 A_sell=None, A_csr=None, device=None, partitioned=False):
+                 A_sell=None, A_csr=None, device=None, partitioned=False, real_pos=None):
         t = require_cuda()
         self.handle = None
         keep = []
@@ -224,6 +224,12 @@ class DevicePlan:
         desc.n = n
         desc.n_real = n_real
         desc.flags = _lib.TB_PLAN_PARTITIONED if partitioned else 0
+        if real_pos is not None and 0 < n_real < n:
+            rp = np.ascontiguousarray(real_pos, dtype=np.int64)
+            if rp.shape[0] != n_real:
+                raise ValueError("real_pos length must equal n_real")
+            keep.append(rp)
+            desc.real_pos = ptr(rp)
         inv = np.ascontiguousarray(inv_d, dtype=np.float64)
         keep.append(inv)
         desc.inv_d = ptr(inv)

@@ -24,8 +24,12 @@ sys.path.insert(0, _REF_SRC)
 import trilab as _ref  # noqa: E402
 import trilab.ordering as _ref_ordering  # noqa: E402
 import trilab.precond as _ref_precond  # noqa: E402
+import trilab._kernels.numba_backend  # noqa: E402,F401  (the verifiers' kernels)
 sys.path.remove(_REF_SRC)
-for _k in [k for k in sys.modules if k == "trilab" or k.startswith("trilab.")]:
+# the reference's kernel package keeps its name (this package has none): the
+# verifiers import their kernels lazily from it
+for _k in [k for k in sys.modules if (k == "trilab" or k.startswith("trilab."))
+           and not k.startswith("trilab._kernels")]:
     sys.modules["_trilab_ref" + _k[len("trilab"):]] = sys.modules.pop(_k)
 
 # at import time: `-p` plugins load before the reference's conftest.py

@@ -108,14 +108,21 @@ def test_shift_changes_history_not_solution(P, grid):
     assert np.linalg.norm(x1 - x0) / np.linalg.norm(x0) < 1e-6
 
 
-def test_hbmc_w1_bitwise_equals_bmc(P):
+@pytest.mark.parametrize("nx,ny,fmt", [(8, 8, "crs"), (5, 5, "crs"), (13, 11, "crs"), (6, 5, "crs"), (30, 22, "crs"),
+                                        (31, 29, "crs"), (5, 5, "sell"), (31, 29, "sell")])
+def test_hbmc_w1_bitwise_equals_bmc(P, nx, ny, fmt):
     """w = 1 makes the HBMC interleave the identity over the padded BMC order
-    (T/test_solver.py:137-145): same iterations, same bits."""
-    a, b = P.gen_laplacian_5pt(8, 8)     # 64 rows, blocks of 4: no dummies
-    xb, rb = P.pcg(a, b, P.CgConfig(ordering="bmc", b_s=4, w=1, spmv_format="crs"))
-    xh, rh = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=4, w=1, spmv_format="crs"))
+    (T/test_solver.py:137-145): with dummy rows (5x5, 13x11, 31x29 grids,
+    blocks of 4) the dot products run over the real rows only, in their
+    order, so iterations, x AND the residual history are bitwise BMC's."""
+    a, b = P.gen_laplacian_5pt(nx, ny)
+    xb, rb = P.pcg(a, b, P.CgConfig(ordering="bmc", b_s=4, w=1, spmv_format=fmt))
+    xh, rh = P.pcg(a, b, P.CgConfig(ordering="hbmc", b_s=4, w=1, spmv_format=fmt))
+    if (nx * ny) % 4:
+        assert rh.n_dummy > 0
     assert rb.iterations == rh.iterations
     assert np.array_equal(xb, xh)
+    assert rb.residual_history == rh.residual_history
 
 
 def test_sell_and_crs_spmv_agree(P, grid):
