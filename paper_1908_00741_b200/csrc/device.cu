@@ -1030,7 +1030,8 @@ struct tb_plan {
     int ring = 0;                  // ring depth (ring kernel)
     size_t smem = 0;
     unsigned grid = 0;
-    int kind = 0;                  // 0 simple, 1 staged task, 2 step ring
+    int kind = 0;                  // 0 simple, 4 lean
+    int block = 256;               // threads per CTA (lean)
   };
   std::vector<ColorLaunch> cl_fwd, cl_bwd;
   int num_sms = 148;
@@ -1130,10 +1131,19 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
       for (long long sid = L.k0 * b_s; sid < L.k1 * b_s; ++sid)
         if (h.slice_len[sid] > lmax) lmax = h.slice_len[sid];
       L.kind = 4;
-      L.max_slots = lmax <= 2 ? 2 : (lmax <= 4 ? 4 : (lmax <= 6 ? 6 : 8));  // KC
-      L.warps = 8;
-      L.smem = sweep_lean::smem_bytes(b_s, kBlock);
-      L.grid = grid_for((L.k1 - L.k0) * w);
+      // KC: slots loaded a step ahead; long rows (w = 32 only) get 12 / 16 /
+      // 24 so the whole slice is in flight (else slots past KC are loaded
+      // one after another inside the step)
+      const long long kcap = env_int("TB_LEAN_KC_MAX", 24);
+      const long long lk = lmax < kcap ? lmax : kcap;
+      L.max_slots = lk <= 2 ? 2 : lk <= 4 ? 4 : lk <= 6 ? 6 : lk <= 8 || w != 32 ? 8
+                  : lk <= 12 ? 12 : lk <= 16 ? 16 : 24;
+      // KC >= 12 kernels hold ~170-250 registers: 128-thread CTAs pack
+      // more warps per SM than 256-thread ones
+      L.block = L.max_slots >= 12 ? env_int("TB_LEAN_BLOCK", 64) : kBlock;
+      L.warps = L.block / 32;
+      L.smem = sweep_lean::smem_bytes(b_s, L.block);
+      L.grid = grid_for((L.k1 - L.k0) * w, L.block);
     }
   }
   static bool attr_done = false;
@@ -1146,6 +1156,12 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
     TB_LEAN_ATTR(true, 2) TB_LEAN_ATTR(true, 4) TB_LEAN_ATTR(true, 6) TB_LEAN_ATTR(true, 8)
     TB_LEAN_ATTR(false, 2) TB_LEAN_ATTR(false, 4) TB_LEAN_ATTR(false, 6) TB_LEAN_ATTR(false, 8)
 #undef TB_LEAN_ATTR
+#define TB_LEAN_ATTR32(F, K)                                                       \
+  CU(cudaFuncSetAttribute(sweep_lean::sweep_kernel<F, K, 32>,                      \
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_optin));
+    TB_LEAN_ATTR32(true, 12) TB_LEAN_ATTR32(true, 16) TB_LEAN_ATTR32(true, 24)
+    TB_LEAN_ATTR32(false, 12) TB_LEAN_ATTR32(false, 16) TB_LEAN_ATTR32(false, 24)
+#undef TB_LEAN_ATTR32
     attr_done = true;
   }
   return TB_OK;
@@ -1161,8 +1177,11 @@ void launch_phase(tb_plan *pl, const tb_plan::ColorLaunch &L, const DevSell &M,
     auto fn = L.max_slots == 2 ? (w32 ? sweep_lean::sweep_kernel<FWD, 2, 32> : sweep_lean::sweep_kernel<FWD, 2, 0>)
               : L.max_slots == 4 ? (w32 ? sweep_lean::sweep_kernel<FWD, 4, 32> : sweep_lean::sweep_kernel<FWD, 4, 0>)
               : L.max_slots == 6 ? (w32 ? sweep_lean::sweep_kernel<FWD, 6, 32> : sweep_lean::sweep_kernel<FWD, 6, 0>)
+              : L.max_slots == 12 ? sweep_lean::sweep_kernel<FWD, 12, 32>
+              : L.max_slots == 16 ? sweep_lean::sweep_kernel<FWD, 16, 32>
+              : L.max_slots == 24 ? sweep_lean::sweep_kernel<FWD, 24, 32>
                                  : (w32 ? sweep_lean::sweep_kernel<FWD, 8, 32> : sweep_lean::sweep_kernel<FWD, 8, 0>);
-    fn<<<L.grid, kBlock, L.smem, s>>>(M.slice_ptr, M.slice_len, M.col, M.val, pl->inv_d, src,
+    fn<<<L.grid, L.block, L.smem, s>>>(M.slice_ptr, M.slice_len, M.col, M.val, pl->inv_d, src,
                                       dst, (int)pl->w, (int)pl->b_s, (int)L.k0, (int)nt,
                                       st ? &st->done : nullptr);
   } else {
@@ -1585,6 +1604,11 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
     lmax = d->L_sell.slice_len[s] > lmax ? d->L_sell.slice_len[s] : lmax;
   for (long long s = 0; s < d->U_sell.n_slices; ++s)
     lmax = d->U_sell.slice_len[s] > lmax ? d->U_sell.slice_len[s] : lmax;
+  // Slices longer than the persistent kernel's 8 register slots (config 3's
+  // 27-point rows, the kNN graph's): the per-phase lean kernels with the
+  // whole slice in flight are as fast or faster (config 3: 832 vs 838 us,
+  // ICCG 49.8 vs 51.5 ms; config 4: 781 vs 950 us; profiles/README.md r02)
+  if (lmax > 8 && env_int("TB_PERSIST_LONG", 0) == 0) return TB_OK;
   const int kc = lmax <= 2 ? 2 : (lmax <= 4 ? 4 : (lmax <= 6 ? 6 : 8));
   const size_t T = persist::kThreads;
   const size_t smem = (size_t)pl->b_s * T * 16 + 8 + 33 * 8 + 64;

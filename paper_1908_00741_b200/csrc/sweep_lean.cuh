@@ -47,6 +47,27 @@ __device__ __forceinline__ double ldv(const double *p) {
   return CG ? __ldcg(p) : __ldg(p);
 }
 
+// Predicated gather as a volatile load: the compiler keeps every gather of
+// a step ahead of the step's first update instead of sinking each one into
+// its slot's branch (which serialises the gathers behind the chain -- seen
+// in the SASS of the KC = 24 kernel: LDG, DMUL, DADD, LDG, ...).  CG: L2
+// only (vectors written by other CTAs inside the launch); else read-only.
+template <bool CG>
+__device__ __forceinline__ double ld_gather(const double *p, bool pred) {
+  double v;
+  if (CG)
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b64 %0, 0;\n"
+        " @q ld.global.cg.f64 %0, [%1];\n}"
+        : "=d"(v) : "l"(p), "r"((int)pred));
+  else
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b64 %0, 0;\n"
+        " @q ld.global.nc.f64 %0, [%1];\n}"
+        : "=d"(v) : "l"(p), "r"((int)pred));
+  return v;
+}
+
 // One lane's b_s-step walk.  W > 0: compile-time slice width; W == 0: w_rt.
 // Shared memory: ys/offs/lens columns of this thread ([b_s][nt] each).
 // dotv != nullptr: also accumulate dotv[row] * result into *dotacc (r . z
@@ -97,7 +118,9 @@ __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_p
 #pragma unroll
     for (int u = 0; u < KC; ++u) {
       const bool inblk = (unsigned)(b.c[u] - blk0) < uspan;
-      x[u] = inblk ? 0.0 : ldv<CG>(dst + b.c[u]);
+      // KC <= 8 (every persistent kernel): ptxas already batches the
+      // gathers, and the volatile form would cost spills at 128 registers
+      x[u] = KC > 8 ? ld_gather<CG>(dst + b.c[u], !inblk) : inblk ? 0.0 : ldv<CG>(dst + b.c[u]);
     }
     double y = b.rhs;
     // branch-free slot update: the shared-memory read is clamped in range
@@ -115,13 +138,40 @@ __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_p
 #pragma unroll
     for (int u = 0; u < KC; ++u)
       if (u < len) update(b.c[u], b.v[u], x[u]);
-    if (len > KC) {  // long row: remaining slots synchronously
+    if (len > KC) {  // long row: the remaining slots
       const int off = offs[i * nt + tid];
-      for (int t = KC; t < len; ++t) {
-        const int cc = __ldg(col + off + t * w);
-        const double vv = __ldg(val + off + t * w);
-        const double xc = (unsigned)(cc - blk0) < uspan ? 0.0 : ldv<CG>(dst + cc);
-        update(cc, vv, xc);
+      if constexpr (KC > 8) {
+        // chunks of 4 with every load of a chunk in flight together
+        // (volatile loads keep ptxas from serialising them behind the chain)
+        for (int t0 = KC; t0 < len; t0 += 4) {
+          int cc[4];
+          double vv[4], xc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool in = t0 + u < len;
+            const int *cp = col + off + (t0 + u) * w;
+            int c;
+            asm volatile(
+                "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b32 %0, %3;\n"
+                " @q ld.global.nc.u32 %0, [%1];\n}"
+                : "=r"(c) : "l"(cp), "r"((int)in), "r"(row));
+            cc[u] = c;
+            vv[u] = ld_gather<false>(val + off + (t0 + u) * w, in);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            xc[u] = ld_gather<CG>(dst + cc[u], (unsigned)(cc[u] - blk0) >= uspan);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (t0 + u < len) update(cc[u], vv[u], xc[u]);
+        }
+      } else {
+        for (int t = KC; t < len; ++t) {
+          const int cc = __ldg(col + off + t * w);
+          const double vv = __ldg(val + off + t * w);
+          const double xc = (unsigned)(cc - blk0) < uspan ? 0.0 : ldv<CG>(dst + cc);
+          update(cc, vv, xc);
+        }
       }
     }
     y = __dmul_rn(y, b.idg);
