@@ -230,7 +230,7 @@ __device__ __forceinline__ void pap_fin(PcgState *st, double pap) {
 // ------------------------------------------------------------ SpMV
 // K/numba_backend.py:26-37: out = 0; out += v * x[col] per slot in stored
 // order.  Optional fused epilogue: pap = p . (A p) and alpha = rz / pap.
-template <bool DOT, bool PAIRED = false>
+template <bool DOT>
 __global__ void __launch_bounds__(kBlock)
     spmv_sell(long long n, const long long *__restrict__ slice_ptr,
               const int *__restrict__ slice_len, const int *__restrict__ col,
@@ -241,14 +241,6 @@ __global__ void __launch_bounds__(kBlock)
   double part = 0.0;
   constexpr int CH = 8;  // slots whose loads / gathers are in flight together
   auto row_fn = [&](long long row) {
-    if (PAIRED) {
-      const long long s = row / w;
-      const double acc = persist::sell_row_paired<4>(val, col, (int)slice_ptr[s], slice_len[s],
-                                                     w, (int)(row - s * w), x);
-      out[row] = acc;
-      if (DOT) part += __ldcg(x + row) * acc;
-      return;
-    }
     const long long s = row / w;
     const int j = (int)(row - s * w);
     const long long off = slice_ptr[s] + j;
@@ -456,13 +448,8 @@ __global__ void __launch_bounds__(kBlock)
   });
 }
 
-// ---- SpMV + p.Ap + alpha + x/r update + ||r|| in ONE cooperative launch
-// (split PCG path).  The TMA SpMV writes ap for this CTA's chunks; a
-// deterministic grid sum (every CTA adds the CTA partials in index order
-// after a grid barrier) gives p.Ap; alpha = rz / p.Ap; the same CTA then
-// updates x and r over the rows it just produced (p and ap are L2-hot) and a
-// second grid sum gives ||r||.  Saves the separate x/r pass's launch and its
-// DRAM re-reads of p and ap.  Semantics of spmv_tma_dot + cg_update_xr.
+// Grid barrier + deterministic grid sum for the cooperative vector kernels
+// (every CTA adds the CTA partials in index order after the barrier).
 __device__ __forceinline__ void coop_sync(unsigned *bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -499,61 +486,6 @@ __device__ __forceinline__ double coop_sum(double v, double *partials, unsigned 
   const double tot = sh[32];
   __syncthreads();
   return tot;
-}
-
-__global__ void __launch_bounds__(spmv_tma::kThreads, 2)
-    spmv_tma_xr(const __grid_constant__ spmv_tma::Params p, double *x, double *r,
-                double *partials, unsigned *bar, PcgState *st, double *hist) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double sh[33];
-  if (st->done) return;   // uniform: every CTA sees the same state
-  spmv_tma::init_bars(p, smem);
-  unsigned phase = 0;
-  const double part = spmv_tma::run<true>(p, smem, phase);
-  const double pap = coop_sum(part, partials, bar, sh);
-  const long long j = st->iter + 1;
-  const double rz = st->rz, bnorm = st->bnorm;
-  if (pap <= 0.0) {  // src/solver.py:176-177
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      st->pap = pap;
-      st->status = TB_ECG_BREAKDOWN;
-      st->bd_iter = j;
-      st->bd_val = pap;
-      stop_loop(st);
-    }
-    return;
-  }
-  const double alpha = rz / pap;
-  // x/r over the rows of this CTA's chunks (the rows run<> produced)
-  double rr = 0.0;
-  const long long rows_per_chunk = (long long)p.S * 32;
-  const long long n = p.n;
-  for (long long q = blockIdx.x; q < p.n_chunks; q += gridDim.x) {
-    const long long r0 = q * rows_per_chunk;
-    const long long r1 = r0 + rows_per_chunk < n ? r0 + rows_per_chunk : n;
-    for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-      const double pi = __ldcg(p.x + i), ai = __ldcg(p.out + i);
-      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
-      const double ri = __dsub_rn(r[i], __dmul_rn(alpha, ai));
-      r[i] = ri;
-      rr += ri * ri;
-    }
-  }
-  const double rrt = coop_sum(rr, partials + gridDim.x, bar, sh);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    st->pap = pap;
-    st->alpha = alpha;
-    const double rel = sqrt(rrt) / bnorm;
-    st->rel = rel;
-    st->iter = j;
-    hist[j] = rel;
-    if (rel < st->tol) {
-      st->converged = 1;
-      stop_loop(st);
-    } else if (j >= st->max_iters) {
-      stop_loop(st);
-    }
-  }
 }
 
 // r . z, beta and p = z + beta p in ONE cooperative launch (src/solver.py:
@@ -696,11 +628,9 @@ __global__ void epoch_bump(unsigned *e) { *e += 1u; }
 // __grid_constant__: device functions take `const Params &`; without it the
 // parameter block would be copied to local memory and every field access
 // would become a local load.
-#ifndef TB_PMINB
-#define TB_PMINB 2   // co-resident CTAs per SM the persistent kernel is built for
-#endif
+constexpr int kPersistMinB = 2;   // co-resident CTAs per SM the persistent kernel is built for
 template <int KC, bool FLOW>
-__global__ void __launch_bounds__(persist::kThreads, TB_PMINB)
+__global__ void __launch_bounds__(persist::kThreads, kPersistMinB)
     pcg_persistent(const __grid_constant__ persist::Params P) {
   extern __shared__ __align__(16) double psm[];
   const int T = blockDim.x, b_s = P.b_s;
@@ -761,7 +691,7 @@ __global__ void __launch_bounds__(persist::kThreads, TB_PMINB)
   for (; j <= max_iters; ++j) {
     if (j == 3) persist::stamp(P, 0);
     const double pap = persist::grid_sum(
-        P, P.a_paired ? persist::spmv_dot_paired(P) : persist::spmv_dot(P), 2, sh);
+        P, persist::spmv_dot(P), 2, sh);
     if (j == 3) persist::stamp(P, 1);
     if (pap <= 0.0) {  // src/solver.py:176-177
       status = TB_ECG_BREAKDOWN;
@@ -822,26 +752,6 @@ __global__ void __launch_bounds__(persist::kThreads, TB_PMINB)
   }
 }
 
-// Preconditioner-only dataflow launch (mode 0, w == 32).  No grid barrier
-// inside (persist.cuh: sweep_pair_dataflow), so it does not share the PCG
-// kernel's register budget: built for TB_PRE_MINB CTAs per SM, which raises
-// the number of lane chains in flight per SM.  Launched cooperatively so the
-// whole grid is co-resident (the flag waits assume every item's warp runs).
-#ifndef TB_PRE_MINB
-#define TB_PRE_MINB 4
-#endif
-template <int KC>
-__global__ void __launch_bounds__(persist::kThreads, TB_PRE_MINB)
-    precond_dataflow(const __grid_constant__ persist::Params P) {
-  extern __shared__ __align__(16) double psm[];
-  const int T = blockDim.x, b_s = P.b_s;
-  double *ys = psm;
-  int *offs = (int *)(ys + (size_t)b_s * T);
-  int *lens = offs + (size_t)b_s * T;
-  persist::sweep_pair_dataflow<KC>(P, P.pre_src, P.y, P.pre_dst, P.epoch, nullptr, ys, offs,
-                                   lens);
-}
-
 // ------------------------------------------------------------ helpers
 inline unsigned grid_for(long long n, int per_block = kBlock) {
   long long g = (n + per_block - 1) / per_block;
@@ -871,7 +781,6 @@ struct DevSell {
   long long *slice_ptr = nullptr;
   int *slice_len = nullptr, *col = nullptr;
   double *val = nullptr;
-  bool paired = false;  // slots stored in the paired layout (upload_sell_paired)
 };
 
 struct DevCsr {
@@ -934,37 +843,6 @@ int upload_sell_step_major(DevSell &d, const tb_sell_host &h,
   if (pos != d.slots) return fail(TB_EINVAL, "step-major upload: slice lengths inconsistent");
   int rc;
   if ((rc = upload(&d.slice_ptr, sp.data(), h.n_slices + 1))) return rc;
-  if ((rc = upload(&d.slice_len, h.slice_len, h.n_slices))) return rc;
-  if ((rc = upload(&d.col, col.data(), d.slots))) return rc;
-  if ((rc = upload(&d.val, val.data(), d.slots))) return rc;
-  return TB_OK;
-}
-
-// Upload a SELL matrix in the PAIRED device layout (persist.cuh:
-// sell_row_paired): inside each slice, slots 2p, 2p+1 of lane j at
-// off + p*2w + 2j, an odd last slot in a tail row at off + (len/2)*2w + j.
-// Same slice offsets and sizes; only the order of slots inside a slice.
-int upload_sell_paired(DevSell &d, const tb_sell_host &h) {
-  d.n_slices = h.n_slices;
-  d.width = h.width;
-  d.slots = h.n_slices > 0 ? h.slice_ptr[h.n_slices] : 0;
-  d.paired = true;
-  const long long w = h.width;
-  std::vector<int> col(d.slots);
-  std::vector<double> val(d.slots);
-  for (long long s = 0; s < h.n_slices; ++s) {
-    const long long off = h.slice_ptr[s], len = h.slice_len[s], np = len / 2;
-    for (long long t = 0; t < len; ++t)
-      for (long long j = 0; j < w; ++j) {
-        const long long src = off + t * w + j;
-        const long long dst = t < 2 * np ? off + (t / 2) * 2 * w + 2 * j + (t & 1)
-                                         : off + np * 2 * w + j;
-        col[dst] = h.col_idx[src];
-        val[dst] = h.vals[src];
-      }
-  }
-  int rc;
-  if ((rc = upload(&d.slice_ptr, (const long long *)h.slice_ptr, h.n_slices + 1))) return rc;
   if ((rc = upload(&d.slice_len, h.slice_len, h.n_slices))) return rc;
   if ((rc = upload(&d.col, col.data(), d.slots))) return rc;
   if ((rc = upload(&d.val, val.data(), d.slots))) return rc;
@@ -1035,7 +913,6 @@ struct tb_plan {
   };
   std::vector<ColorLaunch> cl_fwd, cl_bwd;
   int num_sms = 148;
-  bool step_major = true;  // factor slices stored step-major per color
   // task sweeps
   DevCsr Lc, Uc, Ac;
   DevSched fs, bs;
@@ -1075,14 +952,11 @@ struct tb_plan {
   unsigned epoch = 1;
   // TMA-staged SpMV (spmv_tma.cuh): 0 slices per chunk = not configured
   int spmv_S = 0, spmv_cap = 0, spmv_D = 0, spmv_grid = 0;
-  // precond-only dataflow kernel (0 = use pcg_persistent mode 0)
-  int pre_grid = 0;
 
   // tb_pcg as a host-polled kernel sequence with the TMA SpMV and one
   // persistent dataflow precond launch per iteration (large systems)
   bool split_pcg = false;
   int vec_pt = 16;             // elements per thread of the CG vector kernels (grid size)
-  int xr_grid = 0;             // spmv_tma_xr cooperative grid (0 = separate x/r pass)
   int rzp_grid = 0;            // cg_rz_p_coop cooperative grid (0 = cg_rz + cg_update_p)
   // plans with dummy rows: the real positions (int32, sorted) the CG vector
   // kernels walk (see rloop); n_red = their count (= n without dummies)
@@ -1096,6 +970,24 @@ struct tb_plan {
 
 namespace {
 
+// Execution-path switches, read at plan creation / solve time.  Defaults are
+// the measured-fastest paths; the switches exist so the test suite can force
+// every path (tests/test_gpu_full.py) and for diagnostics -- none changes
+// results beyond the documented +-1 iteration / 1e-10 bar:
+//   TB_PERSIST=0        no persistent kernels (per-phase sweeps, graph PCG)
+//   TB_PERSIST_MIN_N=n  smallest n for the persistent barrier-mode kernel
+//   TB_DATAFLOW=0       barrier-separated color phases instead of per-block flags
+//   TB_FLOW_MAXDEP=n    longest average dependency list for the dataflow schedule
+//   TB_SWEEP=simple     plain thread-per-lane sweep kernel (64-bit offsets)
+//   TB_SPMV_TMA=0       thread-per-row SpMV instead of the TMA-staged one
+//   TB_PCG_SPLIT=0|1    force the split (graph: TMA SpMV + dataflow precond) PCG
+//   TB_PCG_SPLIT_POLL=k split path host-polled every k iterations
+//   TB_PCG_NOGRAPH=k    kernel-sequence PCG host-polled every k iterations
+//   TB_RZP_FUSE=0       separate r.z and p-update kernels
+//   TB_VEC_PAIRS=0      scalar (8-byte) CG vector kernels
+//   TB_L2WIN=0          no L2 persisting window over the CG vectors
+//   TB_DEBUG_SYNC=1     synchronise after every stage of a host-polled iteration
+//   TB_TRACE=1          in-kernel phase timestamps (tb_plan_trace)
 int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return v && *v ? atoi(v) : dflt;
@@ -1134,13 +1026,12 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
       // KC: slots loaded a step ahead; long rows (w = 32 only) get 12 / 16 /
       // 24 so the whole slice is in flight (else slots past KC are loaded
       // one after another inside the step)
-      const long long kcap = env_int("TB_LEAN_KC_MAX", 24);
-      const long long lk = lmax < kcap ? lmax : kcap;
+      const long long lk = lmax < 24 ? lmax : 24;
       L.max_slots = lk <= 2 ? 2 : lk <= 4 ? 4 : lk <= 6 ? 6 : lk <= 8 || w != 32 ? 8
                   : lk <= 12 ? 12 : lk <= 16 ? 16 : 24;
       // KC >= 12 kernels hold ~170-250 registers: 128-thread CTAs pack
       // more warps per SM than 256-thread ones
-      L.block = L.max_slots >= 12 ? env_int("TB_LEAN_BLOCK", 64) : kBlock;
+      L.block = L.max_slots >= 12 ? 64 : kBlock;
       L.warps = L.block / 32;
       L.smem = sweep_lean::smem_bytes(b_s, L.block);
       L.grid = grid_for((L.k1 - L.k0) * w, L.block);
@@ -1280,13 +1171,11 @@ int launch_spmv(tb_plan *pl, const double *x, double *out, cudaStream_t s,
                               spmv_tma::smem_bytes(P.cap, P.D), s>>>(P);
   } else if (pl->spmv_format == TB_SPMV_SELL) {
     if (dot)
-      (pl->A.paired ? spmv_sell<true, true> : spmv_sell<true, false>)
-          <<<reduce_grid(nr, 1), kBlock, 0, s>>>(nr, pl->A.slice_ptr, pl->A.slice_len,
+      spmv_sell<true><<<reduce_grid(nr, 1), kBlock, 0, s>>>(nr, pl->A.slice_ptr, pl->A.slice_len,
                                                  pl->A.col, pl->A.val, (int)pl->A.width, x,
                                                  out, pl->partials, pl->st, pl->rix);
     else
-      (pl->A.paired ? spmv_sell<false, true> : spmv_sell<false, false>)
-          <<<grid_for(n), kBlock, 0, s>>>(n, pl->A.slice_ptr, pl->A.slice_len, pl->A.col,
+      spmv_sell<false><<<grid_for(n), kBlock, 0, s>>>(n, pl->A.slice_ptr, pl->A.slice_len, pl->A.col,
                                           pl->A.val, (int)pl->A.width, x, out, nullptr,
                                           nullptr, nullptr);
   } else {
@@ -1310,7 +1199,7 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
 // the cooperative r.z + p kernel, which then owns that update.
 bool fold_x(const tb_plan *pl) {
   return (pl->n_red % 2) == 0 && env_int("TB_VEC_PAIRS", 1) && pl->rzp_grid > 0 && pl->bar &&
-         env_int("TB_FOLD_X", 1);
+         true;
 }
 
 // The deferred x update of the last iteration (FOLDX solves).
@@ -1351,20 +1240,7 @@ int launch_iteration(tb_plan *pl, double *x, cudaStream_t s, long long *nl) {
   const long long n = pl->n_red;   // the vector kernels' rows (real rows, via pl->rix)
   const unsigned rg = reduce_grid(n, pl->vec_pt);
   int rc;
-  if (pl->split_pcg && pl->xr_grid > 0 && !pl->rix) {
-    spmv_tma::Params P;
-    spmv_params(pl, pl->p, pl->ap, P);
-    double *xx = x, *rr = pl->r, *pp = pl->partials;
-    unsigned *bb = pl->bar;
-    PcgState *ss = pl->st;
-    double *hh = pl->hist;
-    void *args[] = {&P, &xx, &rr, &pp, &bb, &ss, &hh};
-    CU(cudaLaunchCooperativeKernel((const void *)spmv_tma_xr, dim3(pl->xr_grid),
-                                   dim3(spmv_tma::kThreads), args,
-                                   spmv_tma::smem_bytes(P.cap, P.D), s));
-    ++*nl;
-    if ((rc = debug_sync(pl, s, "spmv+xr"))) return rc;
-  } else {
+  {
     if ((rc = launch_spmv(pl, pl->p, pl->ap, s, true, nl))) return rc;
     if ((rc = debug_sync(pl, s, "spmv+dot"))) return rc;
     const bool pairs = (n % 2) == 0 && env_int("TB_VEC_PAIRS", 1);
@@ -1577,16 +1453,6 @@ PersistFn persist_fn(int kc, bool flow) {
   }
 }
 
-using PreFn = void (*)(persist::Params);
-PreFn pre_fn(int kc) {
-  switch (kc) {
-    case 2: return precond_dataflow<2>;
-    case 4: return precond_dataflow<4>;
-    case 6: return precond_dataflow<6>;
-    default: return precond_dataflow<8>;
-  }
-}
-
 // Decide whether the persistent kernel applies and size its cooperative grid.
 int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   pl->persist_ok = false;
@@ -1608,7 +1474,7 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   // 27-point rows, the kNN graph's): the per-phase lean kernels with the
   // whole slice in flight are as fast or faster (config 3: 832 vs 838 us,
   // ICCG 49.8 vs 51.5 ms; config 4: 781 vs 950 us; profiles/README.md r02)
-  if (lmax > 8 && env_int("TB_PERSIST_LONG", 0) == 0) return TB_OK;
+  if (lmax > 8) return TB_OK;
   const int kc = lmax <= 2 ? 2 : (lmax <= 4 ? 4 : (lmax <= 6 ? 6 : 8));
   const size_t T = persist::kThreads;
   const size_t smem = (size_t)pl->b_s * T * 16 + 8 + 33 * 8 + 64;
@@ -1626,10 +1492,7 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
     per_sm = ps < per_sm ? ps : per_sm;
   }
   if (per_sm < 1) return TB_OK;
-  {
-    const int cap = env_int("TB_PERSIST_CTAS", TB_PMINB);
-    if (per_sm > cap) per_sm = cap;
-  }
+  if (per_sm > kPersistMinB) per_sm = kPersistMinB;
   pl->persist_kc = kc;
   pl->persist_smem = smem;
   pl->persist_grid = per_sm * pl->num_sms;
@@ -1698,18 +1561,6 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
       CU(cudaMemset(pl->flags, 0, sizeof(unsigned) * 2 * nl));
       pl->n_lvl1_flow = nl;
       pl->epoch = 1;
-      // the precond-only kernel: its own occupancy (fewer registers)
-      // off by default: measured slower (spills at 64 / 85 registers beat
-      // the extra warps; profiles/README.md) -- TB_PRE_CTAS=n enables it
-      const int cap = env_int("TB_PRE_CTAS", 0);
-      if (cap > 0) {
-        PreFn pf = pre_fn(kc);
-        CU(cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
-        int ps = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, pf, (int)T, smem));
-        if (ps > cap) ps = cap;
-        pl->pre_grid = ps > 0 ? ps * pl->num_sms : 0;
-      }
     }
   }
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
@@ -1780,7 +1631,6 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.Acol = pl->A.col;
   P.Aval = pl->A.val;
   P.aw = (int)(pl->A.width > 0 ? pl->A.width : 1);
-  P.a_paired = pl->A.paired ? 1 : 0;
   P.b = b;
   P.x = x;
   P.r = pl->r;
@@ -1803,21 +1653,9 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
     // a plain one -- the dataflow schedule has no grid barrier, and the
     // graph runs its kernels one after another, so the grid is resident
     P.epoch_dev = pl->epoch_dev;
-    if (env_int("TB_GRAPH_COOP", 0)) {
-      void *a2[] = {&P};
-      CU(cudaLaunchCooperativeKernel((const void *)persist_fn(pl->persist_kc, true),
-                                     dim3(pl->persist_grid), dim3(persist::kThreads), a2,
-                                     pl->persist_smem, s));
-    } else {
-      pcg_persistent_fn_launch(pl, P, s);
-    }
+    pcg_persistent_fn_launch(pl, P, s);
     if (!pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
     CU(cudaGetLastError());
-    return TB_OK;
-  }
-  if (mode == 0 && P.n_lvl1 > 0 && pl->pre_grid > 0) {
-    CU(cudaLaunchCooperativeKernel((const void *)pre_fn(pl->persist_kc), dim3(pl->pre_grid),
-                                   dim3(persist::kThreads), args, pl->persist_smem, s));
     return TB_OK;
   }
   CU(cudaLaunchCooperativeKernel((const void *)persist_fn(pl->persist_kc, P.n_lvl1 > 0),
@@ -1831,23 +1669,10 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
 // = co-resident CTAs.  TB_SPMV_TMA=0 keeps the thread-per-row kernel.
 int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
   pl->spmv_S = 0;
-  if (env_int("TB_SPMV_TMA", 1) == 0 || h.width != 32 || pl->A.paired || h.n_slices <= 0)
+  if (env_int("TB_SPMV_TMA", 1) == 0 || h.width != 32 || h.n_slices <= 0)
     return TB_OK;
   const long long slots = h.slice_ptr[h.n_slices];
   if (slots > 0x7fffffffLL) return TB_OK;
-  // Heavily padded SELL (the kNN graph, 1.35x): the stage would carry the
-  // padding and the scattered gathers dominate -- the thread-per-row kernel
-  // measured faster there (profiles/README.md).
-  long long pad = 0;
-#pragma omp parallel for schedule(static, 1024) reduction(+ : pad)
-  for (long long s = 0; s < h.n_slices; ++s) {
-    const long long off = h.slice_ptr[s];
-    for (long long q = off; q < off + (long long)h.slice_len[s] * 32; ++q)
-      pad += h.vals[q] == 0.0 && h.col_idx[q] == s * 32 + (q - off) % 32;
-  }
-  if (env_int("TB_SPMV_PADRULE", 0) && slots > 0 && (double)slots > 1.2 * (double)(slots - pad))
-    return TB_OK;   // (off: with the 8-slice single-stage candidate the TMA kernel
-                    // also wins on the padded kNN matrix, 404 vs 447 us)
   auto cap_of = [&](int S) {
     long long cap = 0;
     for (long long s0 = 0; s0 < h.n_slices; s0 += S) {
@@ -1865,9 +1690,6 @@ int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
   // with one 16-slice stage at 1 CTA/SM)
   struct Cand { int S, D, kb; };
   Cand cands[4] = {{16, 2, 100}, {8, 1, 100}, {16, 1, 220}, {0, 0, 0}};
-  if (env_int("TB_SPMV_S", 0) > 0)
-    cands[0] = {env_int("TB_SPMV_S", 16), env_int("TB_SPMV_D", 2), env_int("TB_SPMV_KB", 100)},
-    cands[1] = {0, 0, 0};
   int optin = 0;
   CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
   for (const Cand &c : cands) {
@@ -1898,17 +1720,6 @@ int configure_spmv_tma(tb_plan *pl, const tb_sell_host &h) {
     pl->spmv_cap = (int)cap;
     pl->spmv_D = c.D;
     pl->spmv_grid = per_sm * nsm;
-    // fused SpMV + x/r (cooperative): its own co-resident grid
-    if (env_int("TB_XR_FUSE", 0)) {   // off: 26.1 vs 24.5 ms at config 2 (profiles/README.md)
-      cudaFuncAttributes fa;
-      CU(cudaFuncGetAttributes(&fa, spmv_tma_xr));
-      CU(cudaFuncSetAttribute(spmv_tma_xr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              optin - (int)fa.sharedSizeBytes));
-      int ps = 0;
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, spmv_tma_xr, spmv_tma::kThreads, sm));
-      if (ps > per_sm) ps = per_sm;
-      pl->xr_grid = ps > 0 ? ps * nsm : 0;
-    }
     return TB_OK;
   }
   return TB_OK;
@@ -1944,8 +1755,7 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
   pl->spmv_format = d->spmv_format;
   pl->n = d->n;
   pl->n_real = d->n_real;
-  pl->vec_pt = env_int("TB_VEC_PT", 16);   // A/B: 16 > 8 > 4 > 32 (profiles/README.md)
-  if (pl->vec_pt < 1) pl->vec_pt = 1;
+  pl->vec_pt = 16;   // A/B: 16 > 8 > 4 > 32 elements per thread (profiles/README.md)
   int rc = TB_OK;
   auto bail = [&](int code) {
     tb_plan_destroy(pl);
@@ -1960,19 +1770,10 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
     pl->color_lvl1.assign(d->color_lvl1_ranges, d->color_lvl1_ranges + d->n_c + 1);
     if (d->L_sell.width != d->w || d->U_sell.width != d->w)
       return bail(fail(TB_EINVAL, "plan_create: factor slice width != w"));
-    {
-      const char *so = getenv("TB_SLICE_ORDER");
-      pl->step_major = !(so && !strcmp(so, "block"));
-    }
-    if (pl->step_major) {
-      if ((rc = upload_sell_step_major(pl->L, d->L_sell, pl->color_lvl1, d->b_s, false)))
-        return bail(rc);
-      if ((rc = upload_sell_step_major(pl->U, d->U_sell, pl->color_lvl1, d->b_s, true)))
-        return bail(rc);
-    } else {
-      if ((rc = upload_sell(pl->L, d->L_sell))) return bail(rc);
-      if ((rc = upload_sell(pl->U, d->U_sell))) return bail(rc);
-    }
+    if ((rc = upload_sell_step_major(pl->L, d->L_sell, pl->color_lvl1, d->b_s, false)))
+      return bail(rc);
+    if ((rc = upload_sell_step_major(pl->U, d->U_sell, pl->color_lvl1, d->b_s, true)))
+      return bail(rc);
     if ((rc = configure_sweeps(pl, d->L_sell, pl->cl_fwd))) return bail(rc);
     if ((rc = configure_sweeps(pl, d->U_sell, pl->cl_bwd))) return bail(rc);
     if (!(d->flags & TB_PLAN_PARTITIONED) && (rc = configure_persistent(pl, d)))
@@ -1990,10 +1791,7 @@ extern "C" int tb_plan_create(const tb_plan_desc *d, int device, tb_plan **out) 
   } else if (d->spmv_format == TB_SPMV_SELL) {
     if (d->A_sell.n_slices * d->A_sell.width < d->n)
       return bail(fail(TB_EINVAL, "plan_create: SELL A smaller than n"));
-    const bool pair_a = env_int("TB_APAIR", 0) != 0 && d->A_sell.width % 2 == 0 &&
-                        d->A_sell.slice_ptr[d->A_sell.n_slices] <= 0x7fffffffLL;
-    if ((rc = pair_a ? upload_sell_paired(pl->A, d->A_sell) : upload_sell(pl->A, d->A_sell)))
-      return bail(rc);
+    if ((rc = upload_sell(pl->A, d->A_sell))) return bail(rc);
     if ((rc = configure_spmv_tma(pl, d->A_sell))) return bail(rc);
   } else {
     if ((rc = upload_csr(pl->Ac, d->A_csr))) return bail(rc);
@@ -2216,7 +2014,7 @@ extern "C" int tb_plan_persistent(const tb_plan *pl, int32_t *precond, int32_t *
   if (!pl) return fail(TB_EINVAL, "null plan");
   *precond = pl->persist_ok;
   *pcg = pl->persist_ok && pl->persist_pcg_ok;
-  *grid = pl->pre_grid > 0 && pl->n_lvl1_flow > 0 ? pl->pre_grid : pl->persist_grid;
+  *grid = pl->persist_grid;
   return TB_OK;
 }
 
@@ -2267,7 +2065,7 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
   // TB_PCG_SPLIT=1/0 forces it on/off; default: n >= TB_PCG_SPLIT_N.
   {
     const int se = env_int("TB_PCG_SPLIT", -1);
-    const long long sn = (long long)env_int("TB_PCG_SPLIT_N", kSplitN);
+    const long long sn = kSplitN;
     // default whenever the TMA SpMV and the dataflow precond apply
     // (configs 2, 3, 5: 23.3 / 51.9 / 1694 ms vs 28.5 / 54.4 / ~2000 ms for
     // the single persistent launch)

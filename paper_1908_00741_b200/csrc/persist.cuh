@@ -24,21 +24,6 @@
 
 #include "sweep_lean.cuh"
 
-#ifndef TB_FLAG_NS
-#define TB_FLAG_NS 0   // back-off between dependency-flag polls (ns), 0 = spin
-#endif
-#ifndef TB_SMALL_DEPTH
-#define TB_SMALL_DEPTH 2
-#endif
-#ifndef TB_HEAVY_DEPTH
-#define TB_HEAVY_DEPTH 2
-#endif
-#ifndef TB_HEAVY_GA
-#define TB_HEAVY_GA 0
-#endif
-#ifndef TB_PAIR_LAST
-#define TB_PAIR_LAST 0   // A/B: no gain at config 2 or 5 (profiles/README.md)
-#endif
 
 namespace persist {
 
@@ -60,7 +45,6 @@ struct Params {
   const int *Asl, *Acol;
   const double *Aval;
   int aw;
-  int a_paired;           // A stored in the paired layout
   // vectors
   const double *b;
   double *x, *r, *y, *z, *p, *ap;
@@ -219,10 +203,8 @@ __device__ __forceinline__ void wait_flags(const Params &P, const unsigned *flag
     const unsigned *f = flags + dep[q];
     if (ld_relaxed(f) < epoch) {
       const long long t0 = clock64();
-      while (ld_relaxed(f) < epoch) {
-        if (TB_FLAG_NS > 0) __nanosleep(TB_FLAG_NS);
+      while (ld_relaxed(f) < epoch)
         if (clock64() - t0 > P.watchdog) __trap();
-      }
     }
   }
   __syncwarp();
@@ -244,32 +226,16 @@ __device__ __forceinline__ double sweep_pair_dataflow(const Params &P, const dou
   const int n = P.n_lvl1;
   double dot = 0.0;
   // blocks whose slices hold <= 2 slots (e.g. the first color of the forward
-  // sweep: in-block entries only) run the short KC = 2 chain, with a deeper
-  // operand ring (TB_SMALL_DEPTH) since their steps are short
+  // sweep: in-block entries only) run the short KC = 2 chain
   constexpr int KS = KC < 2 ? KC : 2;
-  constexpr int SD = TB_SMALL_DEPTH;
-  constexpr int HD = TB_HEAVY_DEPTH;
-  constexpr bool HG = TB_HEAVY_GA != 0;
-  // Item sequence.  TB_PAIR_LAST (default): [forward items of colors
-  // 0..n_c-2] [(forward k, backward k) pairs of the last color, one warp
-  // doing both back to back] [backward items of colors n_c-2..0, k
-  // descending]: the last color's backward chains (their rhs is the forward
-  // result just written) run interleaved with the heavy forward ones instead
-  // of as a separate, latency-bound wave.  Otherwise forward k ascending then
-  // backward k descending.  Either way every dependency of an item has a
-  // lower sequence index.
-  const int L0 = TB_PAIR_LAST ? P.color_lvl1[P.n_c - 1] : n;
-  const int total = TB_PAIR_LAST ? n + L0 : 2 * n;
   auto fwd_item = [&](int k) {
     wait_flags(P, P.fflag, P.fdep, P.fdep_ptr[k], P.fdep_ptr[k + 1], epoch);
     if (P.small[k] & 1)
-      sweep_lean::lane_chain<true, KS, 32, true, SD>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d,
-                                                     src, mid, 32, P.b_s, k, lane, ys, offs,
-                                                     lens);
+      sweep_lean::lane_chain<true, KS, 32, true>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d, src,
+                                                 mid, 32, P.b_s, k, lane, ys, offs, lens);
     else
-      sweep_lean::lane_chain<true, KC, 32, true, HD, HG>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d,
-                                                         src, mid, 32, P.b_s, k, lane, ys, offs,
-                                                         lens);
+      sweep_lean::lane_chain<true, KC, 32, true>(P.Lsp, P.Lsl, P.Lcol, P.Lval, P.inv_d, src,
+                                                 mid, 32, P.b_s, k, lane, ys, offs, lens);
     __syncwarp();
     if (lane == 0) st_release(P.fflag + k, epoch);
   };
@@ -277,105 +243,27 @@ __device__ __forceinline__ double sweep_pair_dataflow(const Params &P, const dou
     // deps: own rows' rhs (= forward result of block k) + later-color blocks
     wait_flags(P, P.bflag, P.bdep, P.bdep_ptr[k], P.bdep_ptr[k + 1], epoch, P.fflag + k);
     if (P.small[k] & 2)
-      sweep_lean::lane_chain<false, KS, 32, true, SD>(P.Usp, P.Usl, P.Ucol, P.Uval, P.inv_d,
-                                                      mid, dst, 32, P.b_s, k, lane, ys, offs,
-                                                      lens, dotv, &dot);
+      sweep_lean::lane_chain<false, KS, 32, true>(P.Usp, P.Usl, P.Ucol, P.Uval, P.inv_d, mid,
+                                                  dst, 32, P.b_s, k, lane, ys, offs, lens, dotv,
+                                                  &dot);
     else
-      sweep_lean::lane_chain<false, KC, 32, true, HD, HG>(P.Usp, P.Usl, P.Ucol, P.Uval,
-                                                          P.inv_d, mid, dst, 32, P.b_s, k, lane,
-                                                          ys, offs, lens, dotv, &dot);
+      sweep_lean::lane_chain<false, KC, 32, true>(P.Usp, P.Usl, P.Ucol, P.Uval, P.inv_d, mid,
+                                                  dst, 32, P.b_s, k, lane, ys, offs, lens, dotv,
+                                                  &dot);
     __syncwarp();
     if (lane == 0) st_release(P.bflag + k, epoch);
   };
-  for (int it = gw; it < total; it += W) {
-    if (it < L0) {
+  // item sequence: forward k ascending, then backward k descending
+  for (int it = gw; it < 2 * n; it += W) {
+    if (it < n)
       fwd_item(it);
-    } else if (it < n) {
-      if (TB_PAIR_LAST) {
-        fwd_item(it);
-        bwd_item(it);
-      } else {
-        fwd_item(it);
-      }
-    } else {
-      bwd_item(TB_PAIR_LAST ? L0 - 1 - (it - n) : 2 * n - 1 - it);
-    }
+    else
+      bwd_item(2 * n - 1 - it);
   }
   return dot;
 }
 
 // ---------------------------------------------------------------- SpMV
-// Paired SELL (device layout of A, see device.cu:pair_sell): inside a slice
-// of width w and length len, slots 2p and 2p+1 of lane j are adjacent at
-// off + p*2w + 2j (one 16-byte value load, one 8-byte column load); an odd
-// last slot sits in a tail row at off + (len/2)*2w + j.  Same bytes, same
-// slot order, half the load instructions.
-// acc = 0; acc = acc + v*x over the row's slots in order (K/numba_backend.py:26-37).
-template <int MAXP>
-__device__ __forceinline__ double sell_row_paired(const double *__restrict__ vals,
-                                                  const int *__restrict__ cols, int off, int len,
-                                                  int w, int j, const double *x) {
-  double acc = 0.0;
-  const int np = len >> 1;
-  for (int p0 = 0; p0 < np; p0 += MAXP) {
-    double2 v[MAXP];
-    int2 c[MAXP];
-    double x0[MAXP], x1[MAXP];
-#pragma unroll
-    for (int u = 0; u < MAXP; ++u) {
-      const bool in = p0 + u < np;
-      const int o = off + (p0 + u) * 2 * w + 2 * j;
-      v[u] = in ? __ldg((const double2 *)(vals + o)) : make_double2(0.0, 0.0);
-      c[u] = in ? __ldg((const int2 *)(cols + o)) : make_int2(0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < MAXP; ++u) {
-      const bool in = p0 + u < np;
-      x0[u] = in ? __ldcg(x + c[u].x) : 0.0;
-      x1[u] = in ? __ldcg(x + c[u].y) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < MAXP; ++u)
-      if (p0 + u < np) {
-        acc = __dadd_rn(acc, __dmul_rn(v[u].x, x0[u]));
-        acc = __dadd_rn(acc, __dmul_rn(v[u].y, x1[u]));
-      }
-  }
-  if (len & 1) {
-    const int o = off + np * 2 * w + j;
-    acc = __dadd_rn(acc, __dmul_rn(__ldg(vals + o), __ldcg(x + __ldg(cols + o))));
-  }
-  return acc;
-}
-
-// Paired-layout SpMV with the p.Ap partial; two rows per trip (i, i+stride).
-__device__ __forceinline__ double spmv_dot_paired(const Params &P) {
-  const int gthreads = gridDim.x * blockDim.x;
-  double part = 0.0;
-  int row = blockIdx.x * blockDim.x + threadIdx.x;
-  for (; row + gthreads < P.n; row += 2 * gthreads) {
-    const int r1 = row + gthreads;
-    const int s0 = row / P.aw, s1 = r1 / P.aw;
-    const int off0 = (int)P.Asp[s0], off1 = (int)P.Asp[s1];
-    const int len0 = P.Asl[s0], len1 = P.Asl[s1];
-    const double p0 = ldcg(P.p + row), p1 = ldcg(P.p + r1);
-    const double a0 = sell_row_paired<4>(P.Aval, P.Acol, off0, len0, P.aw, row - s0 * P.aw, P.p);
-    const double a1 = sell_row_paired<4>(P.Aval, P.Acol, off1, len1, P.aw, r1 - s1 * P.aw, P.p);
-    P.ap[row] = a0;
-    P.ap[r1] = a1;
-    part += p0 * a0;
-    part += p1 * a1;
-  }
-  for (; row < P.n; row += gthreads) {
-    const int s = row / P.aw;
-    const double a = sell_row_paired<4>(P.Aval, P.Acol, (int)P.Asp[s], P.Asl[s], P.aw,
-                                        row - s * P.aw, P.p);
-    P.ap[row] = a;
-    part += ldcg(P.p + row) * a;
-  }
-  return part;
-}
-
 // ap = A p (K/numba_backend.py:26-37); returns this thread's p.ap partial.
 // Two rows per trip (rows i and i + stride) so two rows' loads and gathers
 // are in flight together; 8 slots per chunk.  Row order of the partial sum

@@ -26,12 +26,6 @@
 
 #pragma once
 
-#ifndef TB_LEAN_MINB
-#define TB_LEAN_MINB 1
-#endif
-#ifndef TB_PF_L2
-#define TB_PF_L2 0
-#endif
 
 namespace sweep_lean {
 
@@ -72,7 +66,7 @@ __device__ __forceinline__ double ld_gather(const double *p, bool pred) {
 // Shared memory: ys/offs/lens columns of this thread ([b_s][nt] each).
 // dotv != nullptr: also accumulate dotv[row] * result into *dotacc (r . z
 // fused into the backward sweep), rows in walk order.
-template <bool FWD, int KC, int W, bool CG, int DEPTH = 2, bool GA = false>
+template <bool FWD, int KC, int W, bool CG>
 __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_ptr,
                                            const int *__restrict__ slice_len,
                                            const int *__restrict__ col,
@@ -180,111 +174,22 @@ __device__ __forceinline__ void lane_chain(const long long *__restrict__ slice_p
     if (dotv) *dotacc += ldv<CG>(dotv + row) * y;
   };
 
-  if constexpr (DEPTH <= 2 && !GA) {
-    Buf<KC> A, B;
-    // TB_PF_L2 = d > 0: at step i, also prefetch into L2 the operand lines of
-    // step i + d (prefetch.global.L2: fire-and-forget, no destination
-    // register), so the register ping-pong's loads hit L2 instead of DRAM.
-    auto prefetch = [&](int i) {
-      if (TB_PF_L2 <= 0 || i >= b_s) return;
-      const int off = offs[i * nt + tid], len = lens[i * nt + tid];
-      const int row = blk0 + (FWD ? i : b_s - 1 - i) * w + j;
-#pragma unroll
-      for (int u = 0; u < KC; ++u)
-        if (u < len) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(val + off + u * w));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(col + off + u * w));
-        }
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(src + row));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(inv_d + row));
-    };
-    if (TB_PF_L2 > 0)
-      for (int q = 1; q <= TB_PF_L2 && q < b_s; ++q) prefetch(q);
-    load(0, A);
-    int i = 0;
-    for (; i + 1 < b_s; i += 2) {
-      prefetch(i + 1 + TB_PF_L2);
-      load(i + 1, B);
-      step(i, A);
-      prefetch(i + 2 + TB_PF_L2);
-      if (i + 2 < b_s) load(i + 2, A);
-      step(i + 1, B);
-    }
-    if (i < b_s) step(i, A);
-  } else {
-    // DEPTH-deep register ring: step i's operands were loaded DEPTH-1 steps
-    // earlier.  GA: the cross-color gathers of step i+1 are also issued
-    // before step i runs (its columns arrived one step earlier), so neither
-    // the operand stream nor the gathers sit on the chain.
-    static_assert(!GA || DEPTH % 2 == 0, "gather-ahead needs an even ring depth");
-    Buf<KC> ring[DEPTH];
-    double xg[GA ? 2 : 1][KC];
-    auto gather = [&](int i, const Buf<KC> &b, double *x) {
-      const int len = lens[i * nt + tid];
-#pragma unroll
-      for (int u = 0; u < KC; ++u) {
-        const bool inblk = (unsigned)(b.c[u] - blk0) < uspan;
-        x[u] = (u < len && !inblk) ? ldv<CG>(dst + b.c[u]) : 0.0;
-      }
-    };
-    auto step_x = [&](int i, const Buf<KC> &b, const double *xc) {
-      const int l = FWD ? i : b_s - 1 - i;
-      const int row = blk0 + l * w + j;
-      const int len = lens[i * nt + tid];
-      double y = b.rhs;
-      auto update = [&](int cc, double vv, double xcross) {
-        const unsigned rel = (unsigned)(cc - blk0);
-        const bool inblk = rel < uspan;
-        unsigned lp = W > 0 ? rel / (unsigned)W : rel / (unsigned)w;
-        lp = lp < (unsigned)b_s ? lp : 0u;
-        const double ysv = ys[(FWD ? (int)lp : b_s - 1 - (int)lp) * nt + tid];
-        const double xin = cc == row ? y : ysv;
-        const double xv = inblk ? xin : xcross;
-        y = __dsub_rn(y, __dmul_rn(vv, xv));
-      };
-#pragma unroll
-      for (int u = 0; u < KC; ++u)
-        if (u < len) update(b.c[u], b.v[u], xc[u]);
-      if (len > KC) {
-        const int off = offs[i * nt + tid];
-        for (int t = KC; t < len; ++t) {
-          const int cc = __ldg(col + off + t * w);
-          const double vv = __ldg(val + off + t * w);
-          const double xcr = (unsigned)(cc - blk0) < uspan ? 0.0 : ldv<CG>(dst + cc);
-          update(cc, vv, xcr);
-        }
-      }
-      y = __dmul_rn(y, b.idg);
-      ys[i * nt + tid] = y;
-      dst[row] = y;
-      if (dotv) *dotacc += ldv<CG>(dotv + row) * y;
-    };
-#pragma unroll
-    for (int d = 0; d < DEPTH - 1; ++d)
-      if (d < b_s) load(d, ring[d]);
-    if (GA) gather(0, ring[0], xg[0]);
-    for (int i0 = 0; i0 < b_s; i0 += DEPTH) {
-#pragma unroll
-      for (int d = 0; d < DEPTH; ++d) {
-        const int i = i0 + d;
-        if (i + DEPTH - 1 < b_s) load(i + DEPTH - 1, ring[(d + DEPTH - 1) % DEPTH]);
-        if (i < b_s) {
-          if (GA) {
-            if (i + 1 < b_s) gather(i + 1, ring[(d + 1) % DEPTH], xg[(d + 1) & 1]);
-            step_x(i, ring[d], xg[d & 1]);
-          } else {
-            double x[KC];
-            gather(i, ring[d], x);
-            step_x(i, ring[d], x);
-          }
-        }
-      }
-    }
+  // operands of step i+1 load while step i gathers and runs its chain: two
+  // register buffers used ping-pong (the loop is unrolled by two)
+  Buf<KC> A, B;
+  load(0, A);
+  int i = 0;
+  for (; i + 1 < b_s; i += 2) {
+    load(i + 1, B);
+    step(i, A);
+    if (i + 2 < b_s) load(i + 2, A);
+    step(i + 1, B);
   }
+  if (i < b_s) step(i, A);
 }
 
 template <bool FWD, int KC, int W>
-__global__ void __launch_bounds__(256, TB_LEAN_MINB)
+__global__ void __launch_bounds__(256, 1)
     sweep_kernel(const long long *__restrict__ slice_ptr, const int *__restrict__ slice_len,
                  const int *__restrict__ col, const double *__restrict__ val,
                  const double *__restrict__ inv_d, const double *__restrict__ src,
@@ -309,7 +214,7 @@ __global__ void __launch_bounds__(256, TB_LEAN_MINB)
 // stores over NVLink), then the last CTA out releases the phase's epoch into
 // every peer's flag for this rank.
 template <bool FWD, int KC>
-__global__ void __launch_bounds__(256, TB_LEAN_MINB)
+__global__ void __launch_bounds__(256, 1)
     sweep_push_kernel(const long long *__restrict__ slice_ptr, const int *__restrict__ slice_len,
                       const int *__restrict__ col, const double *__restrict__ val,
                       const double *__restrict__ inv_d, const double *__restrict__ src,
