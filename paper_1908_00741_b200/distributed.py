@@ -6,15 +6,22 @@ preconditioner application there are `n_c - 1` halo exchanges per sweep --
 one after every color phase that a later phase of the same sweep depends on
 (the reference's `n_c - 1` fork-join barriers, `src/precond.py:389-391`) --
 and one p-halo exchange before each SpMV.  CG dot products are reduced
-across ranks (NCCL all-reduce on the device scalars); the only host read per
-iteration is ‖r‖ for the convergence test, as in `src/solver.py:181-187`.
+across ranks (NCCL all-reduce on the device scalars) at two points per
+iteration: {p.Ap} and {||r||^2, r.z} in one all-reduce; the only host read
+per iteration is p.Ap and ||r|| for the breakdown / convergence tests, as
+in `src/solver.py:176-187`.
 
 The iteration is `src/solver.py:139-204` restated over partitioned vectors:
 
     x0 = 0, r = b, z = M r, p = z, rz = <r, z>
     loop: ap = A p; pap = <p, ap> (<= 0: CgBreakdownError); alpha = rz/pap
-          x += alpha p; r -= alpha ap; rel = ||r||/||b||; stop if rel < tol
-          z = M r; beta = <r, z>/rz; p = z + beta p
+          x += alpha p; r -= alpha ap; z = M r
+          [||r||^2, rz_new] reduced together; rel = ||r||/||b||; stop if rel < tol
+          beta = rz_new/rz; p = z + beta p
+
+M r is applied before the convergence test so that ||r||^2 travels with
+r.z: the values are the reference's, only the last iteration applies M once
+more than the reference does.
 
 Local-rank lockstep: one process may drive several ranks ("virtual ranks",
 e.g. G partitions on one GPU for parity tests, all work serialised on one
@@ -39,8 +46,10 @@ import numpy as np
 from . import _lib
 from .partition import partition_hbmc
 
-# device scalar slots
-BB, PAP, RR, RZ0, RZ1 = 0, 1, 2, 3, 4
+# device scalar slots; r.z alternates between RZ0 and RZ1 around RR, so the
+# merged all-reduce of {||r||^2, r.z_new} is always one contiguous pair and
+# never touches the current r.z
+BB, PAP, RZ0, RR, RZ1 = 0, 1, 2, 3, 4
 N_SCAL = 8
 
 
@@ -172,10 +181,15 @@ class P2PTransport:
 
     NAMES = ("y", "z", "p")
 
-    def __init__(self, drv, fused=True):
+    def __init__(self, drv, fused=True, serialize=False):
         import ctypes as C
         t = drv.ops[0].t
         self.t, self.drv = t, drv
+        # serialize (tests with several processes on ONE GPU): every rank's
+        # pushes complete and all ranks meet at a host barrier before any
+        # rank enqueues a flag wait, so no kernel ever spins on a peer's
+        # kernel (ranks on one GPU are not guaranteed to run concurrently)
+        self.serialize = serialize
         self.world = drv.world
         self.epoch = 0
         self.bufs = []          # per local rank: {name: (ptr, tensor)}
@@ -244,6 +258,11 @@ class P2PTransport:
             self.descs[key] = d = (d, (dptr, dpeer, doff))
         return d[0]
 
+    def _before_wait(self):
+        if self.serialize and self.drv.dist is not None:
+            self.t.cuda.synchronize()
+            self.drv.dist.barrier(group=self.drv.group)
+
     def fused_phase(self, forward, c, src, dst, name):
         """Color phase c of a sweep on every local rank with the halo push
         fused into the sweep kernel, then each rank's stream waits for its
@@ -266,6 +285,7 @@ class P2PTransport:
                                                         self.peer[r]["flags"] + 4 * p.rank,
                                                         self.epoch, self.bufs[i]["ctr"][0], st))
             self.drv.bytes_sent += 8 * int(ex.push_off.shape[0]) if ex.push_off is not None else 0
+        self._before_wait()
         for i, p in enumerate(self.drv.parts):
             _lib.check(_lib.LIB.tb_p2p_wait(self.bufs[i]["flags"][0], self.world, p.rank,
                                             self.epoch, st))
@@ -289,6 +309,7 @@ class P2PTransport:
 
     def wait(self, epoch):
         from . import device as D
+        self._before_wait()
         st = D.current_stream()
         for i, p in enumerate(self.drv.parts):
             _lib.check(_lib.LIB.tb_p2p_wait(self.bufs[i]["flags"][0], self.world, p.rank,
@@ -321,6 +342,7 @@ class P2PTransport:
                     _lib.check(_lib.LIB.tb_p2p_push(0, None, src, None,
                                                     self.peer[d]["flags"] + 4 * p.rank,
                                                     self.epoch, ctr, st))
+        self._before_wait()
         for i, p in enumerate(self.drv.parts):
             _lib.check(_lib.LIB.tb_p2p_wait(self.bufs[i]["flags"][0], self.world, p.rank,
                                             self.epoch, st))
@@ -342,7 +364,7 @@ class DistHbmc:
     per process under torch.distributed, with part.rank == dist rank).
     """
 
-    def __init__(self, parts, ops, group=None, transport="nccl", fused=True):
+    def __init__(self, parts, ops, group=None, transport="nccl", fused=True, serialize=False):
         self.parts = list(parts)
         self.ops = list(ops)
         self.world = self.parts[0].world
@@ -365,7 +387,9 @@ class DistHbmc:
                         self.sendbuf[(key_kind, c, i)] = self.ops[i].vec(ex.n_send)
         self.exchanges = 0
         self.bytes_sent = 0
-        self.p2p = P2PTransport(self, fused=fused) if transport == "p2p" else None
+        self.reductions_per_iteration = 2   # {p.Ap}, {||r||^2, r.z}
+        self.p2p = (P2PTransport(self, fused=fused, serialize=serialize)
+                    if transport == "p2p" else None)
         self._p_epoch = 0
 
     @staticmethod
@@ -443,7 +467,14 @@ class DistHbmc:
                 self.ops[0].add_scal(scals[0], scals[i], slots)
         if self.dist is not None:
             lo, hi = min(slots), max(slots) + 1
-            self.dist.all_reduce(scals[0][lo:hi], group=self.group)
+            assert hi - lo == len(slots), "all-reduced slots must be contiguous"
+            t = scals[0][lo:hi]
+            if t.is_cuda and self.dist.get_backend(self.group) == "gloo":
+                h = t.cpu()   # gloo (one-GPU multi-process tests): via the host
+                self.dist.all_reduce(h, group=self.group)
+                t.copy_(h)
+            else:
+                self.dist.all_reduce(t, group=self.group)
         for i in range(1, len(scals)):
             self.ops[i].set_scal(scals[i], scals[0], slots)
 
@@ -523,7 +554,12 @@ class DistHbmc:
             self.allreduce(sc, [PAP])
             for i in R:
                 O[i].update_xr(sc[i], rz, PAP, p[i], ap[i], x[i], r[i], RR)
-            self.allreduce(sc, [RR])
+            # z = M r before the convergence test: ||r||^2 and r.z are reduced
+            # in one all-reduce (slots RR and rzn are adjacent)
+            self.precond(r, y, z)
+            for i in R:
+                O[i].dot(r[i], z[i], sc[i], rzn)
+            self.allreduce(sc, [RR, rzn])
             pap, rr = O[0].read(sc[0], [PAP, RR])
             if pap <= 0.0:
                 from .solver import CgBreakdownError
@@ -534,10 +570,6 @@ class DistHbmc:
             if rel < tol:
                 converged = True
                 break
-            self.precond(r, y, z)
-            for i in R:
-                O[i].dot(r[i], z[i], sc[i], rzn)
-            self.allreduce(sc, [rzn])
             self.update_p(sc, rzn, rz, z, p)
             rz, rzn = rzn, rz
         return x, it, history, converged
@@ -550,6 +582,62 @@ def partition_setup(setup, world, ranks=None):
     a_sell = csr_to_sell(setup.a_sys, sf.w, want_col64=True)
     return partition_hbmc(sf.lower, sf.upper, a_sell, sf.inv_diag, hl.color_lvl1_ranges,
                           sf.b_s, sf.w, world, ranks)
+
+
+def prepare_rank_parts(a, b, cfg, world, rank=0, dist=None, group=None, shm_root="/dev/shm"):
+    """Rank-local setup: rank 0 alone builds the global HBMC system
+    (solver.prepare -- the greedy ordering and IC(0) are sequential over the
+    whole matrix, src/solver.py:127-136) and partitions it one rank at a
+    time; every rank then loads only its own RankPart and its slice of b
+    from a tmpfs directory (node-local, like the GPUs).  So only rank 0 ever
+    holds the whole system (config 5: ~100 GB of host memory once, not once
+    per rank).  `a` and `b` are only read on rank 0.
+
+    Returns (part, b_loc, info): info on rank 0 = dict(n_pad, old_positions,
+    n_c, n_dummy, t_prepare); on the other ranks the same keys with
+    old_positions None.
+    """
+    import os
+    import pickle
+    import shutil
+    import tempfile
+    from . import solver
+    t0 = time.perf_counter()
+    if dist is None or world == 1:
+        setup = solver.prepare(a, b, cfg)
+        part = partition_setup(setup, world, [rank])[0]
+        return part, setup.b_sys[part.rows], dict(
+            n_pad=setup.a_sys.n, old_positions=setup.old_positions, n_c=setup.n_c,
+            n_dummy=setup.n_dummy, t_prepare=time.perf_counter() - t0)
+    meta = [None]
+    if rank == 0:
+        setup = solver.prepare(a, b, cfg)
+        root = shm_root if os.path.isdir(shm_root) else None
+        tmp = tempfile.mkdtemp(prefix="hbmc_parts_", dir=root)
+        for g in range(world):
+            pg = partition_setup(setup, world, [g])[0]
+            with open(os.path.join(tmp, f"part{g}.pkl"), "wb") as fh:
+                pickle.dump((pg, setup.b_sys[pg.rows]), fh, protocol=5)
+            if g == 0:
+                mine = pg
+            del pg
+        info = dict(n_pad=setup.a_sys.n, old_positions=setup.old_positions, n_c=setup.n_c,
+                    n_dummy=setup.n_dummy)
+        meta = [dict(dir=tmp, n_pad=info["n_pad"], n_c=info["n_c"],
+                     n_dummy=info["n_dummy"])]
+        b0 = setup.b_sys[mine.rows]
+        del setup
+    dist.broadcast_object_list(meta, src=0, group=group)
+    m = meta[0]
+    if rank != 0:
+        with open(os.path.join(m["dir"], f"part{rank}.pkl"), "rb") as fh:
+            mine, b0 = pickle.load(fh)
+        info = dict(n_pad=m["n_pad"], old_positions=None, n_c=m["n_c"], n_dummy=m["n_dummy"])
+    dist.barrier(group=group)
+    if rank == 0:
+        shutil.rmtree(m["dir"], ignore_errors=True)
+    info["t_prepare"] = time.perf_counter() - t0
+    return mine, b0, info
 
 
 def pcg_partitioned(a, b, cfg, world, matrix_name="", group=None, transport="nccl"):
@@ -566,7 +654,6 @@ def pcg_partitioned(a, b, cfg, world, matrix_name="", group=None, transport="ncc
     if cfg.ordering != "hbmc":
         raise ValueError("pcg_partitioned: only the hbmc ordering partitions")
     t0 = time.perf_counter()
-    setup = solver.prepare(a, b, cfg)
     dist = None
     try:
         import torch.distributed as td
@@ -574,35 +661,48 @@ def pcg_partitioned(a, b, cfg, world, matrix_name="", group=None, transport="ncc
             dist = td
     except ImportError:
         pass
-    ranks = [dist.get_rank(group)] if dist is not None else None
     if dist is not None and dist.get_world_size(group) != world:
         raise ValueError("pcg_partitioned: world != torch.distributed world size")
-    parts = partition_setup(setup, world, ranks)
+    if dist is not None:
+        part, b0, info = prepare_rank_parts(a, b, cfg, world, dist.get_rank(group), dist, group)
+        parts, b_hosts = [part], [b0]
+    else:
+        setup = solver.prepare(a, b, cfg)
+        parts = partition_setup(setup, world)
+        b_hosts = [setup.b_sys[p.rows] for p in parts]
+        info = dict(n_pad=setup.a_sys.n, old_positions=setup.old_positions, n_c=setup.n_c,
+                    n_dummy=setup.n_dummy)
+        del setup
     ops = [CudaRankOps(p) for p in parts]
     drv = DistHbmc(parts, ops, group, transport=transport)
-    b_loc = [ops[i].from_host(setup.b_sys[p.rows]) for i, p in enumerate(parts)]
+    b_loc = [ops[i].from_host(bh) for i, bh in enumerate(b_hosts)]
     ops[0].t.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     t1 = time.perf_counter()
-    xs, it, hist, conv = drv.pcg(b_loc, cfg.tol, cfg.max_iters)
-    x_sys = np.zeros(setup.a_sys.n)
-    for i, p in enumerate(parts):
-        x_sys[p.rows] = ops[i].to_host(xs[i])
-    if dist is not None:
-        # every row is owned by exactly one rank: a sum assembles x everywhere
-        xt = ops[0].t.from_numpy(x_sys)
-        if dist.get_backend(group) == "nccl":
-            xt = xt.cuda()
-        dist.all_reduce(xt, group=group)
-        x_sys = xt.cpu().numpy()
+    try:
+        xs, it, hist, conv = drv.pcg(b_loc, cfg.tol, cfg.max_iters)
+        x_sys = np.zeros(info["n_pad"])
+        for i, p in enumerate(parts):
+            x_sys[p.rows] = ops[i].to_host(xs[i])
+        if dist is not None:
+            # every row is owned by exactly one rank: a sum assembles x everywhere
+            xt = ops[0].t.from_numpy(x_sys)
+            if dist.get_backend(group) == "nccl":
+                xt = xt.cuda()
+            dist.all_reduce(xt, group=group)
+            x_sys = xt.cpu().numpy()
+            pos = [info["old_positions"]]
+            dist.broadcast_object_list(pos, src=0, group=group)
+            info["old_positions"] = pos[0]
+    finally:
+        drv.close()
+        for o in ops:
+            o.close()
     t_solve = time.perf_counter() - t1
-    drv.close()
-    for o in ops:
-        o.close()
-    x_out = x_sys[setup.old_positions]
+    x_out = x_sys[info["old_positions"]]
     applies = it if conv else 1 + it
-    barrier_total = applies * 2 * max(setup.n_c - 1, 0)
-    rep = solver.SolveReport(matrix_name, cfg.ordering, cfg.b_s, cfg.w, setup.n_c, int(it),
+    barrier_total = applies * 2 * max(info["n_c"] - 1, 0)
+    rep = solver.SolveReport(matrix_name, cfg.ordering, cfg.b_s, cfg.w, info["n_c"], int(it),
                              bool(conv), t_setup, t_solve, [float(v) for v in hist],
-                             barrier_total, setup.n_dummy)
+                             barrier_total, info["n_dummy"])
     return x_out, rep

@@ -261,3 +261,53 @@ def test_partitioned_pcg_gloo_world2(name, tmp_path):
     m = max(min(len(h), href.shape[0]) - 2, 0)
     assert math.isclose(h[0], href[0])
     assert np.max(np.abs(h[:m] - href[:m]) / href[:m]) <= 1e-6
+
+
+def _gloo_worker_rank_local(rank, world, port, name, out_dir):
+    """Rank-local setup: only rank 0 builds the system; rank r loads its part."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, bs, w, rhs_kind = golden_matrix(name)
+        b = np.ones(a.n) if rhs_kind == "ones" else problems.rhs(a)[1]
+        cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+        if rank != 0:
+            a = b = None   # only rank 0 reads the system
+        part, b_loc, info = D.prepare_rank_parts(a, b, cfg, world, rank, dist,
+                                                 shm_root=out_dir)
+        ops = [OracleRankOps(part)]
+        drv = D.DistHbmc([part], ops)
+        xs, it, hist, conv = drv.pcg([ops[0].from_host(b_loc)], cfg.tol, cfg.max_iters)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), rows=part.rows,
+                 lvals=part.L.vals, x=xs[0][: part.n_loc].numpy(), it=it,
+                 hist=np.asarray(hist), conv=conv, n_pad=info["n_pad"])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32"])
+def test_rank_local_setup_gloo_world2(name, tmp_path):
+    """prepare_rank_parts: rank 1 never builds the system, yet receives
+    exactly the part partition_setup gives it, and the solve meets the bar
+    with 2 reduction points per iteration."""
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_gloo_worker_rank_local, args=(world, _free_port(), name, str(tmp_path)),
+             nprocs=world, join=True)
+    assert not any(p.name.startswith("hbmc_parts_") for p in tmp_path.iterdir())
+    g = load_golden(name)
+    a, b, cfg, st = _setup(name)
+    ref_parts = D.partition_setup(st, world)
+    res = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    for r in range(world):
+        assert np.array_equal(res[r]["rows"], ref_parts[r].rows)
+        assert np.array_equal(res[r]["lvals"], ref_parts[r].L.vals)
+    assert res[0]["it"] == res[1]["it"]
+    x_sys = np.full(int(res[0]["n_pad"]), np.nan)
+    for r in res:
+        x_sys[r["rows"]] = r["x"]
+    x = x_sys[st.old_positions]
+    assert abs(int(res[0]["it"]) - int(g["pcg_hbmc_iters"])) <= 1
+    assert rel_err(x, g["pcg_hbmc_x"]) <= 1e-10
