@@ -51,11 +51,53 @@ def _has_torch():
         return False
 
 
+# ------------------------------------------------------------------ host I/O
+# numpy <-> device copies of large vectors go through a cached pinned buffer:
+# the pageable <-> pinned copies are split over a thread pool (numpy releases
+# the GIL inside copyto) and the DMA runs from / to pinned memory at full
+# link speed.  A caller of apply_ic_preconditioner(numpy r) on config 5 moves
+# 1 GiB each way per call; pageable torch copies did that at ~2 GB/s.
+_STAGE_MIN = 4 << 20          # bytes: smaller vectors take the plain path
+_stage = {"buf": None, "pool": None}
+
+
+def _pinned(nbytes):
+    t = require_cuda()
+    buf = _stage["buf"]
+    if buf is None or buf.numel() < nbytes:
+        _stage["buf"] = buf = t.empty(int(nbytes), dtype=t.uint8, pin_memory=True)
+    return buf
+
+
+def _par_copy(dst, src):
+    """dst[:] = src for 1-D numpy arrays of equal size, split over threads."""
+    import concurrent.futures as cf
+    n = dst.shape[0]
+    k = min(16, os.cpu_count() or 1, max(1, n // (1 << 18)))
+    if k <= 1:
+        np.copyto(dst, src)
+        return
+    if _stage["pool"] is None:
+        _stage["pool"] = cf.ThreadPoolExecutor(max_workers=16)
+    bounds = [n * i // k for i in range(k + 1)]
+    list(_stage["pool"].map(lambda i: np.copyto(dst[bounds[i]:bounds[i + 1]],
+                                                src[bounds[i]:bounds[i + 1]]), range(k)))
+
+
 def to_device(a, dtype=None):
     """numpy -> CUDA tensor (contiguous copy)."""
     t = require_cuda()
     arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
-    return t.from_numpy(arr).to("cuda", non_blocking=False)
+    if arr.nbytes < _STAGE_MIN or arr.ndim != 1:
+        return t.from_numpy(arr).to("cuda", non_blocking=False)
+    pin = _pinned(arr.nbytes)
+    host = pin[: arr.nbytes].numpy().view(arr.dtype)
+    t.cuda.current_stream().synchronize()   # the buffer may still feed a D2H
+    _par_copy(host, arr)
+    out = t.empty(arr.shape[0], dtype=t.from_numpy(arr[:1]).dtype, device="cuda")
+    out.copy_(pin[: arr.nbytes].view(out.dtype), non_blocking=True)
+    t.cuda.current_stream().synchronize()   # the pinned buffer is reused next call
+    return out
 
 
 def empty(n, dtype="f64"):
@@ -88,9 +130,18 @@ def vec_in(x, n):
 
 
 def vec_out(tensor, as_numpy):
-    if as_numpy:
+    if not as_numpy:
+        return tensor
+    t = require_cuda()
+    nbytes = tensor.numel() * tensor.element_size()
+    if nbytes < _STAGE_MIN or tensor.dim() != 1 or not tensor.is_cuda:
         return tensor.cpu().numpy()
-    return tensor
+    pin = _pinned(nbytes)
+    pin[:nbytes].view(tensor.dtype).copy_(tensor, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    out = np.empty(tensor.numel(), dtype=np.dtype(str(tensor.dtype).replace("torch.", "")))
+    _par_copy(out, pin[:nbytes].numpy().view(out.dtype))
+    return out
 
 
 # ------------------------------------------------------------------ matrices
