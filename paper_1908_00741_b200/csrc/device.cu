@@ -39,6 +39,7 @@ using tb::fail;
 #include "sweep_group.cuh"
 #include "spmv_tma.cuh"
 #include "persist.cuh"
+#include "flow2.cuh"
 
 #define CU(call)                                                          \
   do {                                                                    \
@@ -954,6 +955,11 @@ struct tb_plan {
   int *fdep_ptr = nullptr, *fdep = nullptr, *bdep_ptr = nullptr, *bdep = nullptr;
   unsigned *flags = nullptr;  // [2 * n_lvl1]: forward, backward
   unsigned char *small = nullptr;  // per level-1 block: short-chain bits
+  // item-pipelined dataflow kernel (flow2.cuh): unified dependency lists
+  int *dep2 = nullptr, *Lce = nullptr, *Uce = nullptr, *item_k = nullptr;
+  int2 *item_meta = nullptr;
+  int dep_stride = 0, flow2_grid = 0;  // flow2_grid == 0: not configured
+  int flow2_flags = 1;
   unsigned long long *trace = nullptr;  // TB_TRACE=1: in-kernel phase stamps
   unsigned epoch = 1;
   // TMA-staged SpMV (spmv_tma.cuh): 0 slices per chunk = not configured
@@ -1607,6 +1613,104 @@ PersistFn persist_fn(int kc, bool flow) {
   }
 }
 
+PersistFn flow2_fn(int kc) {
+  switch (kc) {
+    case 2: return flow2::precond_kernel<2>;
+    case 4: return flow2::precond_kernel<4>;
+    case 6: return flow2::precond_kernel<6>;
+    default: return flow2::precond_kernel<8>;
+  }
+}
+
+// Item-pipelined dataflow preconditioner (flow2.cuh): one dependency list per
+// item of the sequence [forward k ascending | backward k descending] over
+// the flag array [forward | backward], fixed stride, -1 padded.
+int configure_flow2(tb_plan *pl, int kc, const std::vector<int> &fp, const std::vector<int> &fd,
+                    const std::vector<int> &bp, const std::vector<int> &bd) {
+  pl->flow2_grid = 0;
+  if (env_int("TB_FLOW2", 1) == 0) return TB_OK;
+  const long long nl = pl->n_lvl1_flow, b_s = pl->b_s;
+  if (pl->w != 32 || b_s < 2 || b_s > 32 || (b_s & 1) || nl <= 0) return TB_OK;
+  int ds = 1;
+  for (long long k = 0; k < nl; ++k) {
+    ds = std::max(ds, fp[k + 1] - fp[k]);
+    ds = std::max(ds, bp[k + 1] - bp[k] + 1);
+  }
+  if (ds > 32) return TB_OK;
+  // item order: forward k ascending; backward colors descending, k
+  // ascending inside a color (blocks of one color are independent)
+  std::vector<int> item_k((size_t)2 * nl);
+  for (long long k = 0; k < nl; ++k) item_k[k] = (int)k;
+  {
+    long long it = nl;
+    for (long long c = pl->n_c - 1; c >= 0; --c)
+      for (long long k = pl->color_lvl1[c]; k < pl->color_lvl1[c + 1]; ++k) item_k[it++] = (int)k;
+    if (it != 2 * nl) return TB_OK;
+  }
+  std::vector<int> dep((size_t)2 * nl * ds, -1);
+  for (long long it = 0; it < 2 * nl; ++it) {
+    const long long k = item_k[it];
+    int *o = dep.data() + (size_t)it * ds;
+    if (it < nl) {
+      for (int q = fp[k]; q < fp[k + 1]; ++q) *o++ = fd[q];
+    } else {
+      *o++ = (int)k;  // the backward item's rhs is its own forward block
+      for (int q = bp[k]; q < bp[k + 1]; ++q) *o++ = (int)nl + bd[q];
+    }
+  }
+  int rc;
+  if ((rc = upload(&pl->dep2, dep.data(), (long long)dep.size()))) return rc;
+  if ((rc = upload(&pl->item_k, item_k.data(), (long long)item_k.size()))) return rc;
+  CU(cudaMalloc((void **)&pl->item_meta, sizeof(int2) * (size_t)(2 * nl * b_s)));
+  {
+    const long long cnt = 2 * nl * b_s;
+    flow2::build_item_meta<<<(unsigned)((cnt + 255) / 256), 256>>>(
+        pl->L.slice_ptr, pl->L.slice_len, pl->U.slice_ptr, pl->U.slice_len, pl->item_k,
+        pl->item_meta, (int)nl, (int)b_s);
+    CU(cudaGetLastError());
+  }
+  pl->dep_stride = ds;
+  {
+    // bit 0: L2 bulk prefetch; bits 4-8: distance in steps (<= b_s)
+    const int on = env_int("TB_FLOW2_PF", 1) != 0;
+    int dist = env_int("TB_FLOW2_PFD", 4);
+    dist = dist < 1 ? 1 : (dist > (int)b_s ? (int)b_s : dist);
+    pl->flow2_flags = on | (dist << 4);
+  }
+  // encoded column arrays (in-block / padding slots pre-classified)
+  {
+    int *bad = nullptr;
+    CU(cudaMalloc((void **)&bad, sizeof(int)));
+    CU(cudaMemset(bad, 0, sizeof(int)));
+    for (int f = 0; f < 2; ++f) {
+      const DevSell &M = f ? pl->L : pl->U;
+      int **dst = f ? &pl->Lce : &pl->Uce;
+      CU(cudaMalloc((void **)dst, sizeof(int) * (size_t)(M.slots > 0 ? M.slots : 1)));
+      const unsigned g = (unsigned)((M.n_slices + 7) / 8);
+      if (g) flow2::encode_cols<<<g, 256>>>(M.slice_ptr, M.slice_len, M.col, *dst, M.n_slices,
+                                            (int)b_s, f, bad);
+    }
+    int hbad = 0;
+    CU(cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(bad);
+    if (hbad) {  // an in-block entry outside the lane's own level-2 block: not HBMC
+      cudaFree(pl->Lce);
+      cudaFree(pl->Uce);
+      pl->Lce = pl->Uce = nullptr;
+      return TB_OK;
+    }
+  }
+  PersistFn fn = flow2_fn(kc);
+  const size_t smem = flow2::smem_bytes((int)b_s);
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  int ps = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, flow2::kThreads, smem));
+  if (ps < 1) return TB_OK;
+  if (ps > flow2::kMinBlocks) ps = flow2::kMinBlocks;
+  pl->flow2_grid = ps * pl->num_sms;
+  return TB_OK;
+}
+
 // Decide whether the persistent kernel applies and size its cooperative grid.
 int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   pl->persist_ok = false;
@@ -1715,6 +1819,7 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
       CU(cudaMemset(pl->flags, 0, sizeof(unsigned) * 2 * nl));
       pl->n_lvl1_flow = nl;
       pl->epoch = 1;
+      if ((rc = configure_flow2(pl, kc, fp, fd, bp, bd))) return rc;
     }
   }
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
@@ -1759,6 +1864,13 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
     P.fflag = pl->flags;
     P.bflag = pl->flags + pl->n_lvl1_flow;
     P.small = pl->small;
+    P.dep2 = pl->dep2;
+    P.dep_stride = pl->dep_stride;
+    P.flow2_flags = pl->flow2_flags;
+    P.Lce = pl->Lce;
+    P.Uce = pl->Uce;
+    P.item_meta = pl->item_meta;
+    P.item_k = pl->item_k;
   }
   P.trace = pl->trace;
   {
@@ -1801,6 +1913,16 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.state = pl->st;
   P.watchdog = 4000000000LL;  // ~2 s at 1.9 GHz per barrier wait
   void *args[] = {&P};
+  if (mode == 0 && P.n_lvl1 > 0 && pl->flow2_grid > 0) {
+    // item-pipelined dataflow kernel: no grid barrier, so a plain launch of
+    // the co-resident grid; inside the split PCG graph the epoch comes from
+    // device memory like the persistent kernel's
+    if (pl->in_graph) P.epoch_dev = pl->epoch_dev;
+    flow2_fn(pl->persist_kc)<<<pl->flow2_grid, flow2::kThreads, flow2::smem_bytes(P.b_s), s>>>(P);
+    if (pl->in_graph && !pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
+    CU(cudaGetLastError());
+    return TB_OK;
+  }
   if (mode == 0 && P.n_lvl1 > 0 && pl->in_graph) {
     // captured into the split PCG graph: the epoch comes from device memory
     // (bumped by a 1-thread kernel after each application) and the launch is
@@ -2041,6 +2163,11 @@ extern "C" int tb_plan_destroy(tb_plan *pl) {
   cudaFree(pl->bdep);
   cudaFree(pl->flags);
   cudaFree(pl->small);
+  cudaFree(pl->dep2);
+  cudaFree(pl->Lce);
+  cudaFree(pl->Uce);
+  cudaFree(pl->item_k);
+  cudaFree(pl->item_meta);
   if (pl->ev_in) cudaEventDestroy(pl->ev_in);
   if (pl->ev_out) cudaEventDestroy(pl->ev_out);
   if (pl->stream) cudaStreamDestroy(pl->stream);

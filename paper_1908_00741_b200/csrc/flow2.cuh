@@ -1,0 +1,285 @@
+// Dataflow HBMC preconditioner, pipelined across items (sm_100a).
+//
+// Same schedule and arithmetic as persist::sweep_pair_dataflow (forward
+// level-1 blocks k ascending, then backward k descending, one warp per item,
+// per-block completion flags instead of grid barriers; every product
+// __dmul_rn, every update __dsub_rn, slots in stored order:
+// K/numba_backend.py:132-171), rebuilt around a short instruction stream --
+// the lane chain is latency-bound with 4 warps per scheduler, so every
+// instruction on the per-step path costs wall time:
+//   * pre-classified columns.  The plan keeps an encoded copy of the L / U
+//     column arrays (encode_cols below): a cross-block column stays the row
+//     index (>= 0), an in-block column becomes the shared-memory slot of the
+//     walk step that produced it, a padding slot (col == own row, v == 0)
+//     points at a shared-memory zero.  One generic load per slot then
+//     fetches the operand from global (L2-coherent) or shared memory -- no
+//     range tests, clamps or selects in the chain, which is DMUL + DADD per
+//     slot.  A padding slot is y - 0*y in the reference: the identity except
+//     -0 -> +0 (and inf -> NaN); padding is trailing and that map is
+//     idempotent, so it is applied once after the row's slots when the last
+//     slot is a padding slot (bitwise the reference's result);
+//   * slice lengths are warp-uniform: slots are guarded by uniform branches,
+//     so a short row executes no dead slots;
+//   * the item descriptors (slice offsets / lengths of the b_s steps, the
+//     dependency list) of the NEXT item load while the current one runs and
+//     live in lane registers (lane i holds step i's; read with a shuffle):
+//     no dependent pointer chase or shared-memory staging at item start;
+//   * the operand stream (values, encoded columns, inv_d, rhs) is pulled
+//     into L2 a few steps ahead with cp.async.bulk.prefetch.L2 (two
+//     instructions per step, no registers), across item boundaries;
+//   * flags are polled with ld.acquire (no fence that drains the warp's
+//     outstanding loads).
+// Item order (host-built, item_k): forward blocks k ascending, then the
+// backward sweep color by color (descending) but ASCENDING k inside a color --
+// blocks of one color are independent, and this way a backward item's own
+// forward block (its rhs) finished ~n_lvl1 items ago instead of just now.
+// Dependencies are one unified list per item over the flag array
+// [forward flags | backward flags], fixed stride, -1 padded: a backward item
+// lists its own forward block next to the later-color blocks its U rows read.
+// Every dependency precedes its reader in the item order and each warp walks
+// its items in order, so the lowest unfinished item can always run.
+//
+// w == 32, b_s even and <= 32, every slice <= KC slots, <= 32 dependencies
+// per item (the host checks; otherwise the plan keeps persist.cuh's kernel).
+
+#pragma once
+
+#include "persist.cuh"
+
+namespace flow2 {
+
+#ifndef FLOW2_THREADS
+#define FLOW2_THREADS 256
+#endif
+constexpr int kThreads = FLOW2_THREADS;
+#ifndef FLOW2_PROBE
+#define FLOW2_PROBE 0
+#endif
+#ifndef FLOW2_MINB
+#define FLOW2_MINB 2
+#endif
+constexpr int kMinBlocks = FLOW2_MINB;  // co-resident CTAs per SM the kernel is built for
+constexpr int kInBias = 1 << 30;  // in-block code = walk_step * kThreads - kInBias
+
+// Encoded columns of one factor (warp per slice, lane per row).  fwd: the
+// walk step of in-block source row l' is l'; bwd: b_s-1-l'.
+__global__ void encode_cols(const long long *__restrict__ sp, const int *__restrict__ sl,
+                            const int *__restrict__ col, int *__restrict__ out,
+                            long long n_slices, int b_s, int fwd, int *bad) {
+  const long long sid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (sid >= n_slices) return;
+  const int lane = threadIdx.x & 31;
+  const long long k = sid / b_s;
+  const long long row = sid * 32 + lane;
+  const long long blk0 = k * b_s * 32;
+  const long long off = sp[sid];
+  const int len = sl[sid];
+  for (int t = 0; t < len; ++t) {
+    const long long q = off + (long long)t * 32 + lane;
+    const long long c = col[q];
+    int e;
+    if (c == row) {
+      e = b_s * kThreads - kInBias;  // padding: the zero row
+    } else if (c >= blk0 && c < blk0 + (long long)b_s * 32) {
+      const int ls = (int)((c - blk0) >> 5);
+      if (((c - blk0) & 31) != lane) atomicAdd(bad, 1);  // must be the lane's own level-2 block
+      e = (fwd ? ls : b_s - 1 - ls) * kThreads - kInBias;
+    } else {
+      e = (int)c;
+    }
+    out[q] = e;
+  }
+}
+
+// Per item and walk step: {slice offset, slice length} (lane i of the item's
+// warp loads entry i); item it < n is forward block item_k[it], else backward.
+__global__ void build_item_meta(const long long *__restrict__ Lsp, const int *__restrict__ Lsl,
+                                const long long *__restrict__ Usp, const int *__restrict__ Usl,
+                                const int *__restrict__ item_k, int2 *__restrict__ im, int n,
+                                int b_s) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= 2ll * n * b_s) return;
+  const int it = (int)(g / b_s), i = (int)(g % b_s);
+  const bool fwd = it < n;
+  const long long sid = (long long)item_k[it] * b_s + (fwd ? i : b_s - 1 - i);
+  im[g] = make_int2((int)(fwd ? Lsp : Usp)[sid], (fwd ? Lsl : Usl)[sid]);
+}
+
+template <int KC>
+struct Buf {
+  int e[KC];
+  double v[KC];
+  double rhs, idg;
+};
+
+__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// operand of one slot: generic load (global part L2-coherent), predicated
+__device__ __forceinline__ double ld_operand(const char *addr, bool pred) {
+  double v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+      " @q ld.relaxed.gpu.f64 %0, [%1];\n}"
+      : "=d"(v) : "l"(addr), "r"((int)pred) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void prefetch_line_l2(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// slots U.. of one row: nested warp-uniform branches, so a row of len slots
+// runs len DMUL + DADD pairs and nothing else
+template <int U, int KC>
+__device__ __forceinline__ void chain(int len, double &y, bool &pad, const Buf<KC> &b,
+                                      const double (&x)[KC], int pad_code) {
+  if constexpr (U < KC) {
+    if (len > U) {
+      y = __dsub_rn(y, __dmul_rn(b.v[U], x[U]));
+      pad = b.e[U] == pad_code;
+      chain<U + 1, KC>(len, y, pad, b, x, pad_code);
+    }
+  }
+}
+
+struct Meta {
+  int off, len;  // lane i < b_s: walk step i's slice offset (slots) and length
+  int dep;       // lane q: q-th dependency (index into the flag array) or -1
+  int k;         // the item's level-1 block
+};
+
+template <int KC>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    precond_kernel(const __grid_constant__ persist::Params P) {
+  extern __shared__ __align__(16) double ys_all[];  // [b_s + 1][kThreads]; last row = 0
+  constexpr unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double *ys = ys_all + threadIdx.x;
+  const int NW = gridDim.x * (kThreads >> 5);
+  const int gw = blockIdx.x * (kThreads >> 5) + (threadIdx.x >> 5);
+  const int b_s = P.b_s, n = P.n_lvl1, total = 2 * n;
+  const unsigned epoch = P.epoch_dev ? *P.epoch_dev : P.epoch;
+  const int span = b_s * 32;
+  unsigned *flags = P.fflag;  // [2n]: forward then backward
+  const double *src = P.pre_src;
+  double *mid = P.y, *out = P.pre_dst;
+  const int pad_code = b_s * kThreads - kInBias;
+  // generic address such that base + 8 * code = this thread's ys slot
+  const char *ys_base = (const char *)ys + 8ll * kInBias;
+  ys[b_s * kThreads] = 0.0;
+
+  auto load_meta = [&](int it) {
+    Meta m;
+    int2 ol = make_int2(0, 0);
+    if (lane < b_s) ol = __ldg(P.item_meta + (size_t)it * b_s + lane);
+    m.off = ol.x;
+    m.len = ol.y;
+    m.dep = lane < P.dep_stride ? __ldg(P.dep2 + (size_t)it * P.dep_stride + lane) : -1;
+    m.k = __ldg(P.item_k + it);
+    return m;
+  };
+
+  // static operands of walk step i of item (FWD, k): slots + inv_d (+ rhs
+  // when with_rhs: always safe for forward items and inside an item)
+  auto load_static = [&](bool FWD, int k, int i, const Meta &m, Buf<KC> &b, bool with_rhs) {
+    const int off = __shfl_sync(full, m.off, i) + lane;
+    const int len = __shfl_sync(full, m.len, i);
+    const int row = k * span + (FWD ? i : b_s - 1 - i) * 32 + lane;
+    const int *cp = (FWD ? P.Lce : P.Uce) + off;
+    const double *vp = (FWD ? P.Lval : P.Uval) + off;
+#pragma unroll
+    for (int u0 = 0; u0 < KC; u0 += 2) {
+      if (u0 == 0 || len > u0) {  // warp-uniform
+#pragma unroll
+        for (int u = u0; u < u0 + 2 && u < KC; ++u)
+          if (u < len) {
+            b.e[u] = __ldg(cp + u * 32);
+#if FLOW2_PROBE == 2   // timing probe: no value stream
+            b.v[u] = 1.0;
+#else
+            b.v[u] = __ldg(vp + u * 32);
+#endif
+          }
+      }
+    }
+    b.idg = __ldg(P.inv_d + row);
+    if (with_rhs) b.rhs = FWD ? __ldg(src + row) : __ldcg(mid + row);
+  };
+
+  auto step = [&](bool FWD, int k, int i, const Meta &m, const Buf<KC> &b) {
+    const int row = k * span + (FWD ? i : b_s - 1 - i) * 32 + lane;
+    const int len = __shfl_sync(full, m.len, i);
+    double *dst = FWD ? mid : out;
+    double x[KC];
+#pragma unroll
+    for (int u0 = 0; u0 < KC; u0 += 2) {
+      if (u0 == 0 || len > u0) {  // warp-uniform
+#pragma unroll
+        for (int u = u0; u < u0 + 2 && u < KC; ++u) {
+          const char *base = b.e[u] >= 0 ? (const char *)dst : ys_base;
+#if FLOW2_PROBE == 1   // timing probe: no operand loads
+          x[u] = (double)(long long)(base + 8ll * b.e[u]);
+#elif FLOW2_PROBE == 3  // timing probe: operand loads only for in-block (shared) lanes
+          x[u] = ld_operand(base + 8ll * b.e[u], u < len && b.e[u] < 0);
+#else
+          x[u] = ld_operand(base + 8ll * b.e[u], u < len);
+#endif
+        }
+      }
+    }
+    double y = b.rhs;
+    bool pad = false;
+    chain<0, KC>(len, y, pad, b, x, pad_code);
+    if (pad) y = __dsub_rn(y, __dmul_rn(0.0, y));
+    y = __dmul_rn(y, b.idg);
+    ys[i * kThreads] = y;
+    dst[row] = y;
+  };
+
+  auto wait_deps = [&](const Meta &m) {
+    if (m.dep >= 0) {
+      const unsigned *f = flags + m.dep;
+      if (persist::ld_acquire(f) < epoch) {
+        const long long t0 = clock64();
+        while (persist::ld_acquire(f) < epoch)
+          if (clock64() - t0 > P.watchdog) __trap();
+      }
+    }
+    __syncwarp();
+  };
+
+  if (gw >= total) return;
+  Buf<KC> A, B;
+  Meta cur = load_meta(gw);
+  load_static(gw < n, cur.k, 0, cur, A, gw < n);
+  for (int it = gw; it < total; it += NW) {
+    const bool fwd = it < n;
+    const int k = cur.k;
+    const int itn = it + NW;
+    const bool has_n = itn < total;
+    const bool fwdn = itn < n;
+    Meta nx;
+    nx.off = nx.len = nx.k = 0;
+    nx.dep = -1;
+    if (has_n) nx = load_meta(itn);
+    wait_deps(cur);
+    if (!fwd) A.rhs = __ldcg(mid + k * span + (b_s - 1) * 32 + lane);
+    for (int i = 0; i < b_s; i += 2) {
+      load_static(fwd, k, i + 1, cur, B, true);
+      step(fwd, k, i, cur, A);
+      if (i + 2 < b_s) load_static(fwd, k, i + 2, cur, A, true);
+      step(fwd, k, i + 1, cur, B);
+    }
+    // the next item's first step: its static operands need no flag
+    if (has_n) load_static(fwdn, nx.k, 0, nx, A, fwdn);
+    __syncwarp();
+    if (lane == 0) persist::st_release(flags + (fwd ? k : n + k), epoch);
+    cur = nx;
+  }
+}
+
+__host__ inline size_t smem_bytes(int b_s) { return (size_t)(b_s + 1) * kThreads * 8; }
+
+}  // namespace flow2
