@@ -59,13 +59,14 @@ constexpr int kThreads = FLOW2_THREADS;
 #define FLOW2_MINB 2
 #endif
 constexpr int kMinBlocks = FLOW2_MINB;  // co-resident CTAs per SM the kernel is built for
-constexpr int kInBias = 1 << 30;  // in-block code = walk_step * kThreads - kInBias
+constexpr int kInBias = 1 << 30;  // in-block code = walk_step * (ys row stride) - kInBias
 
 // Encoded columns of one factor (warp per slice, lane per row).  fwd: the
-// walk step of in-block source row l' is l'; bwd: b_s-1-l'.
+// walk step of in-block source row l' is l'; bwd: b_s-1-l'.  stride = doubles
+// between consecutive walk steps' results in the kernel's shared memory.
 __global__ void encode_cols(const long long *__restrict__ sp, const int *__restrict__ sl,
                             const int *__restrict__ col, int *__restrict__ out,
-                            long long n_slices, int b_s, int fwd, int *bad) {
+                            long long n_slices, int b_s, int fwd, int stride, int *bad) {
   const long long sid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (sid >= n_slices) return;
   const int lane = threadIdx.x & 31;
@@ -79,11 +80,11 @@ __global__ void encode_cols(const long long *__restrict__ sp, const int *__restr
     const long long c = col[q];
     int e;
     if (c == row) {
-      e = b_s * kThreads - kInBias;  // padding: the zero row
+      e = b_s * stride - kInBias;  // padding: the zero row
     } else if (c >= blk0 && c < blk0 + (long long)b_s * 32) {
       const int ls = (int)((c - blk0) >> 5);
       if (((c - blk0) & 31) != lane) atomicAdd(bad, 1);  // must be the lane's own level-2 block
-      e = (fwd ? ls : b_s - 1 - ls) * kThreads - kInBias;
+      e = (fwd ? ls : b_s - 1 - ls) * stride - kInBias;
     } else {
       e = (int)c;
     }
@@ -278,6 +279,186 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     if (lane == 0) persist::st_release(flags + (fwd ? k : n + k), epoch);
     cur = nx;
   }
+}
+
+
+// ---------------------------------------------------------------- ring
+// Same item pipeline, with the static operand stream staged through a
+// per-warp shared-memory ring instead of register ping-pong buffers: every
+// step the warp issues the 16-byte cp.async.cg copies of the step D-1 ahead
+// (its slice's values and encoded columns, its inv_d row and -- forward items
+// -- its rhs row), across item boundaries, and consumes the oldest stage with
+// short shared-memory loads.  The copies hold no registers, so D-1 steps of
+// the DRAM stream are in flight per warp where the register version has one,
+// and the step's own dependent latency is the operand gather alone.  A
+// backward item's rhs (the forward result of its own block, valid only after
+// its flag) is prefetched one step ahead in a register instead.
+constexpr int kRingThreads = 128;
+
+template <int KC>
+__host__ __device__ constexpr int ring_stage_bytes() { return KC * 384 + 512; }
+
+__device__ __forceinline__ void cp_async16(unsigned dst, const void *src, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+      " @q cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(dst), "l"(src), "r"((int)pred)
+      : "memory");
+}
+
+template <int KC, int D>
+__global__ void __launch_bounds__(kRingThreads)
+    ring_kernel(const __grid_constant__ persist::Params P) {
+  extern __shared__ __align__(128) unsigned char rsm[];
+  constexpr unsigned full = 0xffffffffu;
+  constexpr int ST = ring_stage_bytes<KC>();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int NW = gridDim.x * (kRingThreads >> 5);
+  const int gw = blockIdx.x * (kRingThreads >> 5) + wib;
+  const int b_s = P.b_s, n = P.n_lvl1, total = 2 * n;
+  const unsigned epoch = P.epoch_dev ? *P.epoch_dev : P.epoch;
+  const int span = b_s * 32;
+  unsigned *flags = P.fflag;
+  const double *src = P.pre_src;
+  double *mid = P.y, *out = P.pre_dst;
+  // per warp: D stages, then ys[b_s + 1][32]
+  const int wbytes = D * ST + (b_s + 1) * 256;
+  unsigned char *wsm = rsm + (size_t)wib * wbytes;
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(wsm);
+  double *ys = (double *)(wsm + D * ST) + lane;
+  const int pad_code = b_s * 32 - kInBias;
+  const char *ys_base = (const char *)ys + 8ll * kInBias;
+  ys[b_s * 32] = 0.0;
+  if (gw >= total) return;
+
+  auto load_meta = [&](int it) {
+    Meta m;
+    int2 ol = make_int2(0, 0);
+    if (lane < b_s) ol = __ldg(P.item_meta + (size_t)it * b_s + lane);
+    m.off = ol.x;
+    m.len = ol.y;
+    m.dep = lane < P.dep_stride ? __ldg(P.dep2 + (size_t)it * P.dep_stride + lane) : -1;
+    m.k = __ldg(P.item_k + it);
+    return m;
+  };
+  auto wait_deps = [&](const Meta &m) {
+    if (m.dep >= 0) {
+      const unsigned *f = flags + m.dep;
+      if (persist::ld_acquire(f) < epoch) {
+        const long long t0 = clock64();
+        while (persist::ld_acquire(f) < epoch)
+          if (clock64() - t0 > P.watchdog) __trap();
+      }
+    }
+    __syncwarp();
+  };
+  // copies of walk step i of item (fwd, m) into ring stage st; one group
+  auto issue = [&](bool valid, bool fwd, const Meta &m, int i, int st) {
+    if (valid) {
+      const int off = __shfl_sync(full, m.off, i);
+      const int len = __shfl_sync(full, m.len, i);
+      const unsigned sb = ring_s + st * ST;
+      const char *vp = (const char *)((fwd ? P.Lval : P.Uval) + off);
+      const char *cp = (const char *)((fwd ? P.Lce : P.Uce) + off);
+#pragma unroll
+      for (int r = 0; r < (KC * 16 + 31) / 32; ++r) {
+        const int c = lane + 32 * r;
+        cp_async16(sb + c * 16, vp + c * 16, c < len * 16);
+      }
+#pragma unroll
+      for (int r = 0; r < (KC * 8 + 31) / 32; ++r) {
+        const int c = lane + 32 * r;
+        cp_async16(sb + KC * 256 + c * 16, cp + c * 16, c < len * 8);
+      }
+      const size_t row0 = (size_t)m.k * span + (fwd ? i : b_s - 1 - i) * 32;
+      // lanes 0-15: inv_d row; lanes 16-31: rhs row (forward: an input)
+      const double *q = lane < 16 ? P.inv_d + row0 + lane * 2 : src + row0 + (lane - 16) * 2;
+      cp_async16(sb + KC * 384 + lane * 16, q, lane < 16 || fwd);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  Meta cur = load_meta(gw);
+  // prologue: steps 0 .. D-2 of the first item (b_s >= D - 1)
+#pragma unroll
+  for (int t = 0; t < D - 1; ++t) issue(true, gw < n, cur, t, t);
+  int st = 0;  // stage of the step about to be consumed
+  for (int it = gw; it < total; it += NW) {
+    const bool fwd = it < n;
+    const int k = cur.k;
+    const int itn = it + NW;
+    const bool has_n = itn < total;
+    const bool fwdn = itn < n;
+    Meta nx;
+    nx.off = nx.len = nx.k = 0;
+    nx.dep = -1;
+    if (has_n) nx = load_meta(itn);
+    wait_deps(cur);
+    double *dst = fwd ? mid : out;
+    double rhs_reg = 0.0;
+    if (!fwd) rhs_reg = __ldcg(mid + (size_t)k * span + (b_s - 1) * 32 + lane);
+    for (int i = 0; i < b_s; ++i) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
+      __syncwarp();
+      {
+        // stream step i + D - 1 (this item's or the next one's) into the
+        // stage consumed last step
+        const int t = i + D - 1;
+        const bool here = t < b_s;
+        int sn = st + D - 1;
+        sn = sn >= D ? sn - D : sn;
+        if (here)
+          issue(true, fwd, cur, t, sn);
+        else
+          issue(has_n, fwdn, nx, t - b_s, sn);
+      }
+      const int len = __shfl_sync(full, cur.len, i);
+      const int row = k * span + (fwd ? i : b_s - 1 - i) * 32 + lane;
+      const unsigned char *sb = wsm + st * ST;
+      const int *se = (const int *)(sb + KC * 256) + lane;
+      const double *sv = (const double *)sb + lane;
+      Buf<KC> b;
+      double x[KC];
+#pragma unroll
+      for (int u0 = 0; u0 < KC; u0 += 2) {
+        if (u0 == 0 || len > u0) {  // warp-uniform
+#pragma unroll
+          for (int u = u0; u < u0 + 2 && u < KC; ++u) {
+            b.e[u] = se[u * 32];
+            const char *base = b.e[u] >= 0 ? (const char *)dst : ys_base;
+            x[u] = ld_operand(base + 8ll * b.e[u], u < len);
+          }
+        }
+      }
+      double rhs_next = 0.0;
+      if (!fwd && i + 1 < b_s) rhs_next = __ldcg(mid + row - 32);
+#pragma unroll
+      for (int u0 = 0; u0 < KC; u0 += 2) {
+        if (u0 == 0 || len > u0) {
+#pragma unroll
+          for (int u = u0; u < u0 + 2 && u < KC; ++u) b.v[u] = sv[u * 32];
+        }
+      }
+      b.idg = *((const double *)(sb + KC * 384) + lane);
+      double y = fwd ? *((const double *)(sb + KC * 384 + 256) + lane) : rhs_reg;
+      bool pad = false;
+      chain<0, KC>(len, y, pad, b, x, pad_code);
+      if (pad) y = __dsub_rn(y, __dmul_rn(0.0, y));
+      y = __dmul_rn(y, b.idg);
+      ys[i * 32] = y;
+      dst[row] = y;
+      rhs_reg = rhs_next;
+      st = st + 1 == D ? 0 : st + 1;
+    }
+    __syncwarp();
+    if (lane == 0) persist::st_release(flags + (fwd ? k : n + k), epoch);
+    cur = nx;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+template <int KC>
+__host__ inline size_t ring_smem_bytes(int b_s, int D) {
+  return (size_t)(kRingThreads / 32) * ((size_t)D * ring_stage_bytes<KC>() + (size_t)(b_s + 1) * 256);
 }
 
 __host__ inline size_t smem_bytes(int b_s) { return (size_t)(b_s + 1) * kThreads * 8; }
