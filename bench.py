@@ -26,9 +26,10 @@ e2e      = the same through the C-ABI plan operator with HOST buffers: pinned
            right-hand sides runs it).  e2e.api = per-call timings of the
            trilab-facing calls a user makes: apply_ic_preconditioner(numpy r)
            (pageable, synchronous) and the ICCG solve b (host) -> x (host).
-roofline = the precond kernel (N = 1: the persistent dataflow kernel, both
-           sweeps in one launch, when the plan has one; else the per-color
-           sweep launches): algorithmic bytes per launch / its CUDA-event
+roofline = the precond kernel (N = 1: the item-pipelined dataflow kernel
+           flow2::precond_kernel, both sweeps in one launch, when the plan
+           has one; else the persistent kernel or the per-color sweep
+           launches): algorithmic bytes per launch / its CUDA-event
            duration, vs MEASURED_PEAKS.json.  `spmv` is the same for the
            plan SpMV.  traffic = ncu dram bytes of that kernel
            (profiles/traffic.json).
@@ -413,7 +414,17 @@ def run_ours(args, rank, world, local_rank):
                           "GBps": nb / (sum(ts) / len(ts) / 1e3) / 1e9})
     peak, peak_src = load_peaks()
     pinfo = plan.persistent()
-    if pinfo["precond"]:
+    finfo = plan.flow_info()
+    if pinfo["precond"] and finfo["grid"] > 0:
+        # the timed step is ONE launch of the item-pipelined dataflow kernel
+        kernel_name = (f"flow2::precond_kernel (csrc/flow2.cuh: one warp per level-1 block, "
+                       f"{finfo['stages']}-stage cp.async ring per warp, per-block completion "
+                       f"flags, no grid barrier; grid {finfo['grid']} x 128 threads, "
+                       f"{finfo['smem']} B smem per CTA)")
+        tot_b = step_bytes * args.steps
+        tot_ms = dev_ms
+        n_launch = args.steps
+    elif pinfo["precond"]:
         # the timed step is ONE persistent launch (both sweeps, all phases)
         kernel_name = (f"pcg_persistent<KC,dataflow> mode=precond (cooperative grid "
                        f"{pinfo['grid']} CTAs, per-level-1-block completion flags, no grid "
@@ -437,7 +448,8 @@ def run_ours(args, rank, world, local_rank):
         if os.path.exists(tp):
             with open(tp) as fh:
                 tj = json.load(fh).get(f"config{args.config}", {})
-            key = "persistent_precond" if pinfo["precond"] else "per_phase"
+            key = ("flow_precond" if pinfo["precond"] and finfo["grid"] > 0 else
+                   "persistent_precond" if pinfo["precond"] else "per_phase")
             if key in tj:
                 traffic = tj[key]["dram_bytes_per_launch"]
                 traffic_src = tj[key]["source"]

@@ -304,6 +304,11 @@ int tb_plan_phase_info(const tb_plan *plan, int forward, int64_t phase,
  * (all color phases separated by in-kernel grid barriers) and its grid. */
 int tb_plan_persistent(const tb_plan *plan, int32_t *precond, int32_t *pcg,
                        int32_t *grid);
+/* Whether tb_plan_precond (and the preconditioner node of the tb_pcg graph)
+ * runs the item-pipelined dataflow kernel (csrc/flow2.cuh): its grid (0 = not
+ * used), ring stages and dynamic shared memory per CTA. */
+int tb_plan_flow_info(const tb_plan *plan, int32_t *grid, int32_t *stages,
+                      int64_t *smem_bytes);
 /* Phase timestamps (%globaltimer, ns) of one steady PCG iteration of the
  * persistent kernel; the plan must be created with TB_TRACE=1 (diagnostics). */
 int tb_plan_trace(const tb_plan *plan, uint64_t *out64 /* [64] */);

@@ -112,6 +112,7 @@ _SIGS = {
     "tb_plan_sweep_phase": [vp, C.c_int, i64, vp, vp, vp],
     "tb_plan_trace": [vp, vp],
     "tb_plan_persistent": [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
+    "tb_plan_flow_info": [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64)],
     "tb_plan_phase_info": [vp, C.c_int, i64, C.POINTER(i32), C.POINTER(i32),
                            C.POINTER(i32), C.POINTER(i32)],
     "tb_pcg": [vp, vp, vp, dbl, i64, i64, vp, C.POINTER(TbPcgReport), vp],

@@ -959,9 +959,7 @@ struct tb_plan {
   int *dep2 = nullptr, *Lce = nullptr, *Uce = nullptr, *item_k = nullptr;
   int2 *item_meta = nullptr;
   int dep_stride = 0, flow2_grid = 0;  // flow2_grid == 0: not configured
-  int flow2_ring_D = 0;                // > 0: shared-memory ring variant, stages
   size_t flow2_smem = 0;
-  int flow2_flags = 1;
   unsigned long long *trace = nullptr;  // TB_TRACE=1: in-kernel phase stamps
   unsigned epoch = 1;
   // TMA-staged SpMV (spmv_tma.cuh): 0 slices per chunk = not configured
@@ -1615,29 +1613,20 @@ PersistFn persist_fn(int kc, bool flow) {
   }
 }
 
-PersistFn flow2_ring_fn(int kc, int D) {
-  switch (kc) {
-    case 2: return D == 4 ? flow2::ring_kernel<2, 4> : flow2::ring_kernel<2, 3>;
-    case 4: return D == 4 ? flow2::ring_kernel<4, 4> : flow2::ring_kernel<4, 3>;
-    case 6: return D == 4 ? flow2::ring_kernel<6, 4> : flow2::ring_kernel<6, 3>;
-    default: return D == 4 ? flow2::ring_kernel<8, 4> : flow2::ring_kernel<8, 3>;
-  }
-}
-size_t flow2_ring_smem(int kc, int b_s, int D) {
-  switch (kc) {
-    case 2: return flow2::ring_smem_bytes<2>(b_s, D);
-    case 4: return flow2::ring_smem_bytes<4>(b_s, D);
-    case 6: return flow2::ring_smem_bytes<6>(b_s, D);
-    default: return flow2::ring_smem_bytes<8>(b_s, D);
-  }
-}
-
 PersistFn flow2_fn(int kc) {
   switch (kc) {
     case 2: return flow2::precond_kernel<2>;
     case 4: return flow2::precond_kernel<4>;
     case 6: return flow2::precond_kernel<6>;
     default: return flow2::precond_kernel<8>;
+  }
+}
+size_t flow2_smem(int kc, int b_s) {
+  switch (kc) {
+    case 2: return flow2::smem_bytes<2>(b_s);
+    case 4: return flow2::smem_bytes<4>(b_s);
+    case 6: return flow2::smem_bytes<6>(b_s);
+    default: return flow2::smem_bytes<8>(b_s);
   }
 }
 
@@ -1649,7 +1638,7 @@ int configure_flow2(tb_plan *pl, int kc, const std::vector<int> &fp, const std::
   pl->flow2_grid = 0;
   if (env_int("TB_FLOW2", 1) == 0) return TB_OK;
   const long long nl = pl->n_lvl1_flow, b_s = pl->b_s;
-  if (pl->w != 32 || b_s < 2 || b_s > 32 || (b_s & 1) || nl <= 0) return TB_OK;
+  if (pl->w != 32 || b_s < flow2::kStages || b_s > 32 || nl <= 0) return TB_OK;
   int ds = 1;
   for (long long k = 0; k < nl; ++k) {
     ds = std::max(ds, fp[k + 1] - fp[k]);
@@ -1689,18 +1678,6 @@ int configure_flow2(tb_plan *pl, int kc, const std::vector<int> &fp, const std::
     CU(cudaGetLastError());
   }
   pl->dep_stride = ds;
-  {
-    // bit 0: L2 bulk prefetch; bits 4-8: distance in steps (<= b_s)
-    const int on = env_int("TB_FLOW2_PF", 1) != 0;
-    int dist = env_int("TB_FLOW2_PFD", 4);
-    dist = dist < 1 ? 1 : (dist > (int)b_s ? (int)b_s : dist);
-    pl->flow2_flags = on | (dist << 4);
-  }
-  // variant: shared-memory ring of D stages (TB_FLOW2_RING=0: register
-  // ping-pong buffers); needs D - 1 <= b_s
-  int ring_D = env_int("TB_FLOW2_RING", 1) ? env_int("TB_FLOW2_D", 3) : 0;
-  if (ring_D > 0) ring_D = ring_D >= 4 ? 4 : 3;
-  if (ring_D - 1 > (int)b_s) ring_D = 0;
   // encoded column arrays (in-block / padding slots pre-classified)
   {
     int *bad = nullptr;
@@ -1712,7 +1689,7 @@ int configure_flow2(tb_plan *pl, int kc, const std::vector<int> &fp, const std::
       CU(cudaMalloc((void **)dst, sizeof(int) * (size_t)(M.slots > 0 ? M.slots : 1)));
       const unsigned g = (unsigned)((M.n_slices + 7) / 8);
       if (g) flow2::encode_cols<<<g, 256>>>(M.slice_ptr, M.slice_len, M.col, *dst, M.n_slices,
-                                            (int)b_s, f, ring_D > 0 ? 32 : flow2::kThreads, bad);
+                                            (int)b_s, f, 32, bad);
     }
     int hbad = 0;
     CU(cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1724,30 +1701,15 @@ int configure_flow2(tb_plan *pl, int kc, const std::vector<int> &fp, const std::
       return TB_OK;
     }
   }
-  if (ring_D > 0) {
-    PersistFn fn = flow2_ring_fn(kc, ring_D);
-    const size_t smem = flow2_ring_smem(kc, (int)b_s, ring_D);
-    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    int ps = 0;
-    if (smem <= 200 * 1024)
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, flow2::kRingThreads, smem));
-    const int cap = env_int("TB_FLOW2_CTAS", 0);
-    if (cap > 0 && ps > cap) ps = cap;
-    if (ps >= 1) {
-      pl->flow2_ring_D = ring_D;
-      pl->flow2_smem = smem;
-      pl->flow2_grid = ps * pl->num_sms;
-      return TB_OK;
-    }
-    return TB_OK;  // (the encoded columns use the ring's stride: no register variant)
-  }
   PersistFn fn = flow2_fn(kc);
-  const size_t smem = flow2::smem_bytes((int)b_s);
-  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  const size_t smem = flow2_smem(kc, (int)b_s);
+  int optin = 0;
+  CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
+  if (smem > (size_t)optin) return TB_OK;
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int ps = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, flow2::kThreads, smem));
   if (ps < 1) return TB_OK;
-  if (ps > flow2::kMinBlocks) ps = flow2::kMinBlocks;
   pl->flow2_smem = smem;
   pl->flow2_grid = ps * pl->num_sms;
   return TB_OK;
@@ -1908,7 +1870,6 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
     P.small = pl->small;
     P.dep2 = pl->dep2;
     P.dep_stride = pl->dep_stride;
-    P.flow2_flags = pl->flow2_flags;
     P.Lce = pl->Lce;
     P.Uce = pl->Uce;
     P.item_meta = pl->item_meta;
@@ -1960,11 +1921,7 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
     // the co-resident grid; inside the split PCG graph the epoch comes from
     // device memory like the persistent kernel's
     if (pl->in_graph) P.epoch_dev = pl->epoch_dev;
-    if (pl->flow2_ring_D > 0)
-      flow2_ring_fn(pl->persist_kc, pl->flow2_ring_D)<<<pl->flow2_grid, flow2::kRingThreads,
-                                                        pl->flow2_smem, s>>>(P);
-    else
-      flow2_fn(pl->persist_kc)<<<pl->flow2_grid, flow2::kThreads, pl->flow2_smem, s>>>(P);
+    flow2_fn(pl->persist_kc)<<<pl->flow2_grid, flow2::kThreads, pl->flow2_smem, s>>>(P);
     if (pl->in_graph && !pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
     CU(cudaGetLastError());
     return TB_OK;
@@ -2342,6 +2299,15 @@ extern "C" int tb_plan_persistent(const tb_plan *pl, int32_t *precond, int32_t *
   *precond = pl->persist_ok;
   *pcg = pl->persist_ok && pl->persist_pcg_ok;
   *grid = pl->persist_grid;
+  return TB_OK;
+}
+
+extern "C" int tb_plan_flow_info(const tb_plan *pl, int32_t *grid, int32_t *stages,
+                                 int64_t *smem_bytes) {
+  if (!pl) return fail(TB_EINVAL, "null plan");
+  *grid = pl->flow2_grid;
+  *stages = pl->flow2_grid > 0 ? flow2::kStages : 0;
+  *smem_bytes = pl->flow2_grid > 0 ? (int64_t)pl->flow2_smem : 0;
   return TB_OK;
 }
 

@@ -1,46 +1,57 @@
-// Dataflow HBMC preconditioner, pipelined across items (sm_100a).
+// Dataflow HBMC preconditioner, one software pipeline per warp (sm_100a).
 //
-// Same schedule and arithmetic as persist::sweep_pair_dataflow (forward
-// level-1 blocks k ascending, then backward k descending, one warp per item,
-// per-block completion flags instead of grid barriers; every product
-// __dmul_rn, every update __dsub_rn, slots in stored order:
-// K/numba_backend.py:132-171), rebuilt around a short instruction stream --
-// the lane chain is latency-bound with 4 warps per scheduler, so every
-// instruction on the per-step path costs wall time:
+// Schedule and arithmetic are those of persist::sweep_pair_dataflow: one warp
+// per item (a level-1 block of the forward or of the backward sweep), one
+// lane per level-2 block walking its b_s rows, per-block completion flags
+// instead of grid barriers; every product __dmul_rn, every update __dsub_rn,
+// slots in stored order (K/numba_backend.py:132-171) -- bitwise the
+// reference's z.  The lane chain is latency-bound (a few warps per
+// scheduler, each a dependent instruction stream), so the kernel is built to
+// keep the DRAM stream in flight without registers and the per-step
+// instruction stream short:
+//   * static operands through a per-warp shared-memory ring.  Every step the
+//     warp issues the 16-byte cp.async.cg copies of the step D-1 ahead (its
+//     slice's values and encoded columns, its inv_d row and -- forward items
+//     -- its rhs row), across item boundaries, and consumes the oldest stage
+//     with short shared-memory loads.  The copies hold no registers, so D-1
+//     steps of the stream are in flight per warp (register ping-pong buffers
+//     hold one), and ~20 warps fit per SM;
 //   * pre-classified columns.  The plan keeps an encoded copy of the L / U
-//     column arrays (encode_cols below): a cross-block column stays the row
-//     index (>= 0), an in-block column becomes the shared-memory slot of the
-//     walk step that produced it, a padding slot (col == own row, v == 0)
-//     points at a shared-memory zero.  One generic load per slot then
-//     fetches the operand from global (L2-coherent) or shared memory -- no
-//     range tests, clamps or selects in the chain, which is DMUL + DADD per
-//     slot.  A padding slot is y - 0*y in the reference: the identity except
-//     -0 -> +0 (and inf -> NaN); padding is trailing and that map is
-//     idempotent, so it is applied once after the row's slots when the last
-//     slot is a padding slot (bitwise the reference's result);
+//     column arrays (encode_cols): a cross-block column stays the row index
+//     (>= 0), an in-block column becomes the shared-memory slot of the walk
+//     step that produced it, a padding slot (col == own row, v == 0) points at
+//     a shared-memory zero.  One generic load per slot fetches the operand
+//     from global (L2-coherent) or shared memory -- no range tests, clamps or
+//     selects; the chain is DMUL + DADD per slot.  A padding slot is y - 0*y
+//     in the reference: the identity except -0 -> +0 (and inf -> NaN);
+//     padding is trailing and that map is idempotent, so it is applied once
+//     after the row's slots when the last slot is a padding slot;
 //   * slice lengths are warp-uniform: slots are guarded by uniform branches,
 //     so a short row executes no dead slots;
 //   * the item descriptors (slice offsets / lengths of the b_s steps, the
-//     dependency list) of the NEXT item load while the current one runs and
-//     live in lane registers (lane i holds step i's; read with a shuffle):
-//     no dependent pointer chase or shared-memory staging at item start;
-//   * the operand stream (values, encoded columns, inv_d, rhs) is pulled
-//     into L2 a few steps ahead with cp.async.bulk.prefetch.L2 (two
-//     instructions per step, no registers), across item boundaries;
-//   * flags are polled with ld.acquire (no fence that drains the warp's
-//     outstanding loads).
+//     dependency list, the block index) of the NEXT item load while the
+//     current one runs and live in lane registers (lane i holds step i's;
+//     read with a shuffle): no pointer chase at item start;
+//   * flags are polled with ld.acquire (no fence that would drain the
+//     warp's outstanding copies); a backward item's rhs (the forward result
+//     of its own block, valid only after its flag) is prefetched one step
+//     ahead in a register instead of through the ring.
 // Item order (host-built, item_k): forward blocks k ascending, then the
 // backward sweep color by color (descending) but ASCENDING k inside a color --
 // blocks of one color are independent, and this way a backward item's own
-// forward block (its rhs) finished ~n_lvl1 items ago instead of just now.
+// forward block finished ~n_lvl1 items ago instead of just now.
 // Dependencies are one unified list per item over the flag array
 // [forward flags | backward flags], fixed stride, -1 padded: a backward item
 // lists its own forward block next to the later-color blocks its U rows read.
 // Every dependency precedes its reader in the item order and each warp walks
 // its items in order, so the lowest unfinished item can always run.
 //
-// w == 32, b_s even and <= 32, every slice <= KC slots, <= 32 dependencies
-// per item (the host checks; otherwise the plan keeps persist.cuh's kernel).
+// Requirements (host-checked; otherwise the plan keeps persist.cuh's kernel):
+// w == 32, kStages <= b_s <= 32, every slice <= KC <= 8 slots, <= 32
+// dependencies per item, in-block entries only inside a lane's own level-2
+// block.  What was tried and rejected on the way (profiles/README.md r02q-x):
+// register ping-pong buffers, L2 prefetch (bulk and per line), 3-4 CTAs/SM
+// with spills, gathers issued one step ahead, lazy flag publication.
 
 #pragma once
 
@@ -48,17 +59,6 @@
 
 namespace flow2 {
 
-#ifndef FLOW2_THREADS
-#define FLOW2_THREADS 256
-#endif
-constexpr int kThreads = FLOW2_THREADS;
-#ifndef FLOW2_PROBE
-#define FLOW2_PROBE 0
-#endif
-#ifndef FLOW2_MINB
-#define FLOW2_MINB 2
-#endif
-constexpr int kMinBlocks = FLOW2_MINB;  // co-resident CTAs per SM the kernel is built for
 constexpr int kInBias = 1 << 30;  // in-block code = walk_step * (ys row stride) - kInBias
 
 // Encoded columns of one factor (warp per slice, lane per row).  fwd: the
@@ -113,10 +113,6 @@ struct Buf {
   double rhs, idg;
 };
 
-__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 // operand of one slot: generic load (global part L2-coherent), predicated
 __device__ __forceinline__ double ld_operand(const char *addr, bool pred) {
   double v;
@@ -125,10 +121,6 @@ __device__ __forceinline__ double ld_operand(const char *addr, bool pred) {
       " @q ld.relaxed.gpu.f64 %0, [%1];\n}"
       : "=d"(v) : "l"(addr), "r"((int)pred) : "memory");
   return v;
-}
-
-__device__ __forceinline__ void prefetch_line_l2(const void *p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // slots U.. of one row: nested warp-uniform branches, so a row of len slots
@@ -151,149 +143,9 @@ struct Meta {
   int k;         // the item's level-1 block
 };
 
-template <int KC>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-    precond_kernel(const __grid_constant__ persist::Params P) {
-  extern __shared__ __align__(16) double ys_all[];  // [b_s + 1][kThreads]; last row = 0
-  constexpr unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  double *ys = ys_all + threadIdx.x;
-  const int NW = gridDim.x * (kThreads >> 5);
-  const int gw = blockIdx.x * (kThreads >> 5) + (threadIdx.x >> 5);
-  const int b_s = P.b_s, n = P.n_lvl1, total = 2 * n;
-  const unsigned epoch = P.epoch_dev ? *P.epoch_dev : P.epoch;
-  const int span = b_s * 32;
-  unsigned *flags = P.fflag;  // [2n]: forward then backward
-  const double *src = P.pre_src;
-  double *mid = P.y, *out = P.pre_dst;
-  const int pad_code = b_s * kThreads - kInBias;
-  // generic address such that base + 8 * code = this thread's ys slot
-  const char *ys_base = (const char *)ys + 8ll * kInBias;
-  ys[b_s * kThreads] = 0.0;
-
-  auto load_meta = [&](int it) {
-    Meta m;
-    int2 ol = make_int2(0, 0);
-    if (lane < b_s) ol = __ldg(P.item_meta + (size_t)it * b_s + lane);
-    m.off = ol.x;
-    m.len = ol.y;
-    m.dep = lane < P.dep_stride ? __ldg(P.dep2 + (size_t)it * P.dep_stride + lane) : -1;
-    m.k = __ldg(P.item_k + it);
-    return m;
-  };
-
-  // static operands of walk step i of item (FWD, k): slots + inv_d (+ rhs
-  // when with_rhs: always safe for forward items and inside an item)
-  auto load_static = [&](bool FWD, int k, int i, const Meta &m, Buf<KC> &b, bool with_rhs) {
-    const int off = __shfl_sync(full, m.off, i) + lane;
-    const int len = __shfl_sync(full, m.len, i);
-    const int row = k * span + (FWD ? i : b_s - 1 - i) * 32 + lane;
-    const int *cp = (FWD ? P.Lce : P.Uce) + off;
-    const double *vp = (FWD ? P.Lval : P.Uval) + off;
-#pragma unroll
-    for (int u0 = 0; u0 < KC; u0 += 2) {
-      if (u0 == 0 || len > u0) {  // warp-uniform
-#pragma unroll
-        for (int u = u0; u < u0 + 2 && u < KC; ++u)
-          if (u < len) {
-            b.e[u] = __ldg(cp + u * 32);
-#if FLOW2_PROBE == 2   // timing probe: no value stream
-            b.v[u] = 1.0;
-#else
-            b.v[u] = __ldg(vp + u * 32);
-#endif
-          }
-      }
-    }
-    b.idg = __ldg(P.inv_d + row);
-    if (with_rhs) b.rhs = FWD ? __ldg(src + row) : __ldcg(mid + row);
-  };
-
-  auto step = [&](bool FWD, int k, int i, const Meta &m, const Buf<KC> &b) {
-    const int row = k * span + (FWD ? i : b_s - 1 - i) * 32 + lane;
-    const int len = __shfl_sync(full, m.len, i);
-    double *dst = FWD ? mid : out;
-    double x[KC];
-#pragma unroll
-    for (int u0 = 0; u0 < KC; u0 += 2) {
-      if (u0 == 0 || len > u0) {  // warp-uniform
-#pragma unroll
-        for (int u = u0; u < u0 + 2 && u < KC; ++u) {
-          const char *base = b.e[u] >= 0 ? (const char *)dst : ys_base;
-#if FLOW2_PROBE == 1   // timing probe: no operand loads
-          x[u] = (double)(long long)(base + 8ll * b.e[u]);
-#elif FLOW2_PROBE == 3  // timing probe: operand loads only for in-block (shared) lanes
-          x[u] = ld_operand(base + 8ll * b.e[u], u < len && b.e[u] < 0);
-#else
-          x[u] = ld_operand(base + 8ll * b.e[u], u < len);
-#endif
-        }
-      }
-    }
-    double y = b.rhs;
-    bool pad = false;
-    chain<0, KC>(len, y, pad, b, x, pad_code);
-    if (pad) y = __dsub_rn(y, __dmul_rn(0.0, y));
-    y = __dmul_rn(y, b.idg);
-    ys[i * kThreads] = y;
-    dst[row] = y;
-  };
-
-  auto wait_deps = [&](const Meta &m) {
-    if (m.dep >= 0) {
-      const unsigned *f = flags + m.dep;
-      if (persist::ld_acquire(f) < epoch) {
-        const long long t0 = clock64();
-        while (persist::ld_acquire(f) < epoch)
-          if (clock64() - t0 > P.watchdog) __trap();
-      }
-    }
-    __syncwarp();
-  };
-
-  if (gw >= total) return;
-  Buf<KC> A, B;
-  Meta cur = load_meta(gw);
-  load_static(gw < n, cur.k, 0, cur, A, gw < n);
-  for (int it = gw; it < total; it += NW) {
-    const bool fwd = it < n;
-    const int k = cur.k;
-    const int itn = it + NW;
-    const bool has_n = itn < total;
-    const bool fwdn = itn < n;
-    Meta nx;
-    nx.off = nx.len = nx.k = 0;
-    nx.dep = -1;
-    if (has_n) nx = load_meta(itn);
-    wait_deps(cur);
-    if (!fwd) A.rhs = __ldcg(mid + k * span + (b_s - 1) * 32 + lane);
-    for (int i = 0; i < b_s; i += 2) {
-      load_static(fwd, k, i + 1, cur, B, true);
-      step(fwd, k, i, cur, A);
-      if (i + 2 < b_s) load_static(fwd, k, i + 2, cur, A, true);
-      step(fwd, k, i + 1, cur, B);
-    }
-    // the next item's first step: its static operands need no flag
-    if (has_n) load_static(fwdn, nx.k, 0, nx, A, fwdn);
-    __syncwarp();
-    if (lane == 0) persist::st_release(flags + (fwd ? k : n + k), epoch);
-    cur = nx;
-  }
-}
-
-
-// ---------------------------------------------------------------- ring
-// Same item pipeline, with the static operand stream staged through a
-// per-warp shared-memory ring instead of register ping-pong buffers: every
-// step the warp issues the 16-byte cp.async.cg copies of the step D-1 ahead
-// (its slice's values and encoded columns, its inv_d row and -- forward items
-// -- its rhs row), across item boundaries, and consumes the oldest stage with
-// short shared-memory loads.  The copies hold no registers, so D-1 steps of
-// the DRAM stream are in flight per warp where the register version has one,
-// and the step's own dependent latency is the operand gather alone.  A
-// backward item's rhs (the forward result of its own block, valid only after
-// its flag) is prefetched one step ahead in a register instead.
-constexpr int kRingThreads = 128;
+// ---------------------------------------------------------------- kernel
+constexpr int kThreads = 128;
+constexpr int kStages = 3;  // ring depth (4: fewer warps fit, slower at b_s = 16)
 
 template <int KC>
 __host__ __device__ constexpr int ring_stage_bytes() { return KC * 384 + 512; }
@@ -305,15 +157,16 @@ __device__ __forceinline__ void cp_async16(unsigned dst, const void *src, bool p
       : "memory");
 }
 
-template <int KC, int D>
-__global__ void __launch_bounds__(kRingThreads)
-    ring_kernel(const __grid_constant__ persist::Params P) {
+template <int KC>
+__global__ void __launch_bounds__(kThreads)
+    precond_kernel(const __grid_constant__ persist::Params P) {
   extern __shared__ __align__(128) unsigned char rsm[];
   constexpr unsigned full = 0xffffffffu;
+  constexpr int D = kStages;
   constexpr int ST = ring_stage_bytes<KC>();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int NW = gridDim.x * (kRingThreads >> 5);
-  const int gw = blockIdx.x * (kRingThreads >> 5) + wib;
+  const int NW = gridDim.x * (kThreads >> 5);
+  const int gw = blockIdx.x * (kThreads >> 5) + wib;
   const int b_s = P.b_s, n = P.n_lvl1, total = 2 * n;
   const unsigned epoch = P.epoch_dev ? *P.epoch_dev : P.epoch;
   const int span = b_s * 32;
@@ -456,11 +309,11 @@ __global__ void __launch_bounds__(kRingThreads)
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-template <int KC>
-__host__ inline size_t ring_smem_bytes(int b_s, int D) {
-  return (size_t)(kRingThreads / 32) * ((size_t)D * ring_stage_bytes<KC>() + (size_t)(b_s + 1) * 256);
-}
 
-__host__ inline size_t smem_bytes(int b_s) { return (size_t)(b_s + 1) * kThreads * 8; }
+template <int KC>
+__host__ inline size_t smem_bytes(int b_s) {
+  return (size_t)(kThreads / 32) *
+         ((size_t)kStages * ring_stage_bytes<KC>() + (size_t)(b_s + 1) * 256);
+}
 
 }  // namespace flow2

@@ -66,7 +66,6 @@ struct Params {
   // flow2.cuh: per item of [forward | backward] a -1 padded dependency list
   const int *dep2;
   int dep_stride;
-  int flow2_flags;  // bit 0: L2 bulk prefetch on; bits 4-8: prefetch distance (steps)
   const int *Lce, *Uce;  // encoded column arrays (flow2::encode_cols)
   const int2 *item_meta;  // [2 n_lvl1][b_s] {slice offset, length} per item and walk step
   const int *item_k;      // [2 n_lvl1] level-1 block of each item

@@ -357,6 +357,12 @@ class DevicePlan:
         check(LIB.tb_plan_persistent(self.handle, *vals))
         return dict(zip(("precond", "pcg", "grid"), (v.value for v in vals)))
 
+    def flow_info(self):
+        """Item-pipelined dataflow preconditioner kernel: grid (0 = not used), stages, smem."""
+        g, st, sm = _lib.i32(), _lib.i32(), _lib.i64()
+        check(LIB.tb_plan_flow_info(self.handle, g, st, sm))
+        return {"grid": g.value, "stages": st.value, "smem": sm.value}
+
     def barriers_per_sweep(self):
         v = _lib.i64()
         check(LIB.tb_plan_barriers_per_sweep(self.handle, v))

@@ -463,13 +463,13 @@ def test_kernel_seam_concurrent_ranges(P):
 
 @pytest.mark.parametrize("name", ["knn3000_b4_w32", "var7_16_b8_w32", "s27_10_b8_w32",
                                   "aniso12_b16_w32", "lap7_12_b4_w8"])
-@pytest.mark.parametrize("env", [{}, {"TB_DATAFLOW": "0"}, {"TB_PERSIST": "0"},
+@pytest.mark.parametrize("env", [{}, {"TB_FLOW2": "0"}, {"TB_DATAFLOW": "0"}, {"TB_PERSIST": "0"},
                                  {"TB_PERSIST": "0", "TB_SWEEP": "simple"},
                                  {"TB_PERSIST_MIN_N": "0"}, {"TB_FLOW_MAXDEP": "0"}])
 def test_every_precond_path_bitwise(P, name, env, monkeypatch):
-    """Every internal schedule of the preconditioner (dataflow persistent,
-    barrier persistent, per-phase lean / simple kernels) gives the
-    reference's z bit for bit."""
+    """Every internal schedule of the preconditioner (item-pipelined dataflow
+    kernel, dataflow persistent, barrier persistent, per-phase lean / simple
+    kernels) gives the reference's z bit for bit."""
     import torch
     from paper_1908_00741_b200 import solver
     for k, v in env.items():
@@ -483,6 +483,63 @@ def test_every_precond_path_bitwise(P, name, env, monkeypatch):
     st.plan.precond(r, z)
     torch.cuda.synchronize()
     assert np.array_equal(z.cpu().numpy(), g["z"])
+    st.plan.close()
+
+
+@pytest.mark.parametrize("name,expect", [("var7_16_b8_w32", True), ("aniso12_b16_w32", True),
+                                         ("lap7_12_b4_w8", False),
+                                         ("s27_10_b8_w32", False)])
+def test_flow_kernel_selection(P, name, expect):
+    """The item-pipelined dataflow kernel (csrc/flow2.cuh) runs exactly where
+    its preconditions hold: w = 32, slices of at most 8 slots, at most 32
+    dependencies per level-1 block; TB_FLOW2=0 leaves the persistent kernel."""
+    from paper_1908_00741_b200 import solver
+    try:
+        a, bs, w, _ = golden_matrix(name)
+    except Exception:
+        pytest.skip("golden not present")
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    st = solver.attach_plan(solver.prepare(a, np.zeros(a.n), cfg), cfg)
+    info = st.plan.flow_info()
+    if expect is not None:
+        assert (info["grid"] > 0) == expect, info
+    if info["grid"] > 0:
+        assert info["stages"] == 3 and 0 < info["smem"] <= 227 * 1024
+    st.plan.close()
+
+
+def test_flow_kernel_signed_zero_and_padding_rule(P):
+    """Padding slots are y - 0*y in the reference (identity except -0 -> +0).
+    The flow kernel applies that map once per padded row; rows of a right-hand
+    side full of +0 / -0 / tiny values must still match the oracle bit for
+    bit, sign of zero included."""
+    import torch
+    from oracle import oracle as O
+    from paper_1908_00741_b200 import solver
+    name = "var7_16_b8_w32"
+    a, bs, w, _ = golden_matrix(name)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=w, spmv_format="sell")
+    st = solver.attach_plan(solver.prepare(a, np.zeros(a.n), cfg), cfg)
+    assert st.plan.flow_info()["grid"] > 0
+    ob = O.HbmcSystem(O.Csr(a.n, a.row_ptr, a.col_idx, a.vals), np.zeros(a.n), bs, w)
+    n = st.layout.n_pad
+    rng = np.random.default_rng(5)
+    for trial in range(4):
+        r = rng.standard_normal(n)
+        m = rng.integers(0, 4, n)
+        r[m == 0] = 0.0
+        r[m == 1] = -0.0
+        if trial >= 2:
+            r[m == 2] = 5e-324 * rng.integers(-3, 4, int((m == 2).sum()))
+        if trial == 3:
+            r[:] = np.where(rng.integers(0, 2, n) == 0, 0.0, -0.0)
+        rt = torch.from_numpy(r).cuda()
+        z = torch.full_like(rt, float("nan"))
+        st.plan.precond(rt, z)
+        torch.cuda.synchronize()
+        yo = O.hbmc_sweep(True, ob.Ls, ob.inv_d, r, ob.hl)
+        zo = O.hbmc_sweep(False, ob.Us, ob.inv_d, yo, ob.hl)
+        assert np.array_equal(z.cpu().numpy().view(np.int64), zo.view(np.int64))
     st.plan.close()
 
 
