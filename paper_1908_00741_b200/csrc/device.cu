@@ -1914,7 +1914,10 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.bar_count = pl->bar;
   P.bar_gen = pl->bar + 1;
   P.state = pl->st;
-  P.watchdog = 4000000000LL;  // ~2 s at 1.9 GHz per barrier wait
+  // per-wait watchdog of the in-kernel barriers / flag polls: traps (a sticky
+  // context error) instead of hanging the GPU; TB_WATCHDOG_MS=0 disables it
+  // (hosts that time-slice the GPU), default ~2 s
+  P.watchdog = (long long)env_int("TB_WATCHDOG_MS", 2000) * 1900000LL;
   void *args[] = {&P};
   if (mode == 0 && P.n_lvl1 > 0 && pl->flow2_grid > 0) {
     // item-pipelined dataflow kernel: no grid barrier, so a plain launch of

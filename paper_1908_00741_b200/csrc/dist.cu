@@ -20,6 +20,7 @@
 // streaming: 16 B/row (dot), 48 B/row (x/r update), 24 B/row (p update).
 
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <cstring>
 
@@ -202,7 +203,7 @@ __global__ void wait_kernel(const unsigned *flags, int count, int skip, unsigned
       unsigned v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + q) : "memory");
       if ((int)(v - epoch) >= 0) break;
-      if (clock64() - t0 > watchdog) __trap();
+      if (watchdog > 0 && clock64() - t0 > watchdog) __trap();
     }
   }
 }
@@ -298,7 +299,13 @@ extern "C" int tb_p2p_push(int64_t n, const int32_t *idx, const double *src, dou
 extern "C" int tb_p2p_wait(const uint32_t *flags, int32_t count, int32_t skip, uint32_t epoch,
                            void *stream) {
   if (count <= 0) return TB_OK;
-  wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flags, count, skip, epoch, 8000000000LL);
+  // watchdog as in device.cu: TB_WATCHDOG_MS (default 2000; the peer wait gets
+  // twice that), 0 disables the trap
+  static const long long wd = [] {
+    const char *e = getenv("TB_WATCHDOG_MS");
+    return (long long)(e && *e ? atoi(e) : 2000) * 2 * 1900000LL;
+  }();
+  wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flags, count, skip, epoch, wd);
   CU(cudaGetLastError());
   return TB_OK;
 }

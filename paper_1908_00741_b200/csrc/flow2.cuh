@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads)
       if (persist::ld_acquire(f) < epoch) {
         const long long t0 = clock64();
         while (persist::ld_acquire(f) < epoch)
-          if (clock64() - t0 > P.watchdog) __trap();
+          if (P.watchdog > 0 && clock64() - t0 > P.watchdog) __trap();
       }
     }
     __syncwarp();

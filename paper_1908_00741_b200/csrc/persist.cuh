@@ -98,7 +98,7 @@ __device__ __forceinline__ void grid_sync(const Params &P) {
     } else {
       const long long t0 = clock64();
       while (*gen == g) {
-        if (clock64() - t0 > P.watchdog) __trap();
+        if (P.watchdog > 0 && clock64() - t0 > P.watchdog) __trap();
       }
     }
     __threadfence();
@@ -203,14 +203,14 @@ __device__ __forceinline__ void wait_flags(const Params &P, const unsigned *flag
   if (extra && lane == 0 && ld_relaxed(extra) < epoch) {
     const long long t0 = clock64();
     while (ld_relaxed(extra) < epoch)
-      if (clock64() - t0 > P.watchdog) __trap();
+      if (P.watchdog > 0 && clock64() - t0 > P.watchdog) __trap();
   }
   for (int q = d0 + lane; q < d1; q += 32) {
     const unsigned *f = flags + dep[q];
     if (ld_relaxed(f) < epoch) {
       const long long t0 = clock64();
       while (ld_relaxed(f) < epoch)
-        if (clock64() - t0 > P.watchdog) __trap();
+        if (P.watchdog > 0 && clock64() - t0 > P.watchdog) __trap();
     }
   }
   __syncwarp();
