@@ -415,7 +415,7 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_src = load_peaks()
     pinfo = plan.persistent()
     finfo = plan.flow_info()
-    if pinfo["precond"] and finfo["grid"] > 0:
+    if finfo["grid"] > 0:
         # the timed step is ONE launch of the item-pipelined dataflow kernel
         kernel_name = (f"flow2::precond_kernel (csrc/flow2.cuh: one warp per level-1 block, "
                        f"{finfo['stages']}-stage cp.async ring per warp, per-block completion "
@@ -448,7 +448,7 @@ def run_ours(args, rank, world, local_rank):
         if os.path.exists(tp):
             with open(tp) as fh:
                 tj = json.load(fh).get(f"config{args.config}", {})
-            key = ("flow_precond" if pinfo["precond"] and finfo["grid"] > 0 else
+            key = ("flow_precond" if finfo["grid"] > 0 else
                    "persistent_precond" if pinfo["precond"] else "per_phase")
             if key in tj:
                 traffic = tj[key]["dram_bytes_per_launch"]

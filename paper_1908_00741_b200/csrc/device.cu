@@ -960,6 +960,7 @@ struct tb_plan {
   int2 *item_meta = nullptr;
   int dep_stride = 0, flow2_grid = 0;  // flow2_grid == 0: not configured
   size_t flow2_smem = 0;
+  bool flow2_long = false;  // slices longer than 8 slots: chunked ring stages
   unsigned long long *trace = nullptr;  // TB_TRACE=1: in-kernel phase stamps
   unsigned epoch = 1;
   // TMA-staged SpMV (spmv_tma.cuh): 0 slices per chunk = not configured
@@ -1613,12 +1614,13 @@ PersistFn persist_fn(int kc, bool flow) {
   }
 }
 
-PersistFn flow2_fn(int kc) {
+PersistFn flow2_fn(int kc, bool long_slices) {
+  if (long_slices) return flow2::precond_kernel<8, true>;
   switch (kc) {
-    case 2: return flow2::precond_kernel<2>;
-    case 4: return flow2::precond_kernel<4>;
-    case 6: return flow2::precond_kernel<6>;
-    default: return flow2::precond_kernel<8>;
+    case 2: return flow2::precond_kernel<2, false>;
+    case 4: return flow2::precond_kernel<4, false>;
+    case 6: return flow2::precond_kernel<6, false>;
+    default: return flow2::precond_kernel<8, false>;
   }
 }
 size_t flow2_smem(int kc, int b_s) {
@@ -1633,7 +1635,7 @@ size_t flow2_smem(int kc, int b_s) {
 // Item-pipelined dataflow preconditioner (flow2.cuh): one dependency list per
 // item of the sequence [forward k ascending | backward k descending] over
 // the flag array [forward | backward], fixed stride, -1 padded.
-int configure_flow2(tb_plan *pl, int kc, const std::vector<int> &fp, const std::vector<int> &fd,
+int configure_flow2(tb_plan *pl, int kc, bool long_slices, const std::vector<int> &fp, const std::vector<int> &fd,
                     const std::vector<int> &bp, const std::vector<int> &bd) {
   pl->flow2_grid = 0;
   if (env_int("TB_FLOW2", 1) == 0) return TB_OK;
@@ -1701,7 +1703,7 @@ int configure_flow2(tb_plan *pl, int kc, const std::vector<int> &fp, const std::
       return TB_OK;
     }
   }
-  PersistFn fn = flow2_fn(kc);
+  PersistFn fn = flow2_fn(kc, long_slices);
   const size_t smem = flow2_smem(kc, (int)b_s);
   int optin = 0;
   CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
@@ -1711,6 +1713,8 @@ int configure_flow2(tb_plan *pl, int kc, const std::vector<int> &fp, const std::
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, flow2::kThreads, smem));
   if (ps < 1) return TB_OK;
   pl->flow2_smem = smem;
+  pl->flow2_long = long_slices;
+  pl->persist_kc = kc;
   pl->flow2_grid = ps * pl->num_sms;
   return TB_OK;
 }
@@ -1733,11 +1737,16 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   for (long long s = 0; s < d->U_sell.n_slices; ++s)
     lmax = d->U_sell.slice_len[s] > lmax ? d->U_sell.slice_len[s] : lmax;
   // Slices longer than the persistent kernel's 8 register slots (config 3's
-  // 27-point rows, the kNN graph's): the per-phase lean kernels with the
-  // whole slice in flight are as fast or faster (config 3: 832 vs 838 us,
-  // ICCG 49.8 vs 51.5 ms; config 4: 781 vs 950 us; profiles/README.md r02)
-  if (lmax > 8) return TB_OK;
+  // 27-point rows, the kNN graph's): no persistent kernel -- the per-phase
+  // lean kernels with the whole slice in flight are as fast or faster
+  // (config 3: 832 vs 838 us; config 4: 781 vs 950 us; profiles/README.md
+  // r02) -- but the item-pipelined dataflow kernel (flow2.cuh, chunked ring
+  // stages) still applies when the dependency lists are short (config 3).
+  const bool long_slices = lmax > 8;
+  if (long_slices && (pl->w != 32 || env_int("TB_FLOW2", 1) == 0)) return TB_OK;
   const int kc = lmax <= 2 ? 2 : (lmax <= 4 ? 4 : (lmax <= 6 ? 6 : 8));
+  int rc;
+  if (!long_slices) {
   const size_t T = persist::kThreads;
   const size_t smem = (size_t)pl->b_s * T * 16 + 8 + 33 * 8 + 64;
   int v = 0;
@@ -1759,12 +1768,12 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
   pl->persist_smem = smem;
   pl->persist_grid = per_sm * pl->num_sms;
   std::vector<int> cl(pl->color_lvl1.begin(), pl->color_lvl1.end());
-  int rc;
   if ((rc = upload(&pl->color_lvl1_dev, cl.data(), (long long)cl.size()))) return rc;
   CU(cudaMalloc((void **)&pl->bar, 2 * sizeof(unsigned)));
   CU(cudaMemset(pl->bar, 0, 2 * sizeof(unsigned)));
   CU(cudaMalloc((void **)&pl->ppartials, sizeof(double) * persist::kSlots * pl->persist_grid));
   pl->persist_ok = true;
+  }
   // ---- dataflow sweeps (w == 32): level-1 block dependency lists.  Every
   // cross-block column of a forward row must lie in an EARLIER level-1
   // block and of a backward row in a LATER one (HBMC structure); otherwise
@@ -1797,6 +1806,8 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
         }
         std::sort(tmp.begin(), tmp.end());
         tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+        // long slices only run the flow kernel: <= 32 entries per item
+        if (long_slices && tmp.size() > 31) ok = false;
         dep.insert(dep.end(), tmp.begin(), tmp.end());
         ptr[k + 1] = (int)dep.size();
       }
@@ -1823,9 +1834,12 @@ int configure_persistent(tb_plan *pl, const tb_plan_desc *d) {
       CU(cudaMemset(pl->flags, 0, sizeof(unsigned) * 2 * nl));
       pl->n_lvl1_flow = nl;
       pl->epoch = 1;
-      if ((rc = configure_flow2(pl, kc, fp, fd, bp, bd))) return rc;
+      if ((rc = configure_flow2(pl, kc, long_slices, fp, fd, bp, bd))) return rc;
+      // without the persistent kernels the flags only serve the flow kernel
+      if (long_slices && pl->flow2_grid == 0) pl->n_lvl1_flow = 0;
     }
   }
+  if (long_slices) return TB_OK;
   pl->persist_pcg_ok = d->spmv_format == TB_SPMV_SELL;
   // Without the dataflow schedule a small system runs faster as per-phase
   // kernels in a CUDA graph (config 1: ICCG 2.01 vs 2.44 ms, precond 36 vs
@@ -1924,7 +1938,8 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
     // the co-resident grid; inside the split PCG graph the epoch comes from
     // device memory like the persistent kernel's
     if (pl->in_graph) P.epoch_dev = pl->epoch_dev;
-    flow2_fn(pl->persist_kc)<<<pl->flow2_grid, flow2::kThreads, pl->flow2_smem, s>>>(P);
+    flow2_fn(pl->persist_kc, pl->flow2_long)<<<pl->flow2_grid, flow2::kThreads, pl->flow2_smem,
+                                               s>>>(P);
     if (pl->in_graph && !pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
     CU(cudaGetLastError());
     return TB_OK;
@@ -2217,7 +2232,9 @@ extern "C" int tb_plan_backward(tb_plan *pl, const double *y, double *z, void *s
 extern "C" int tb_plan_precond(tb_plan *pl, const double *r, double *z, void *stream) {
   if (!pl) return fail(TB_EINVAL, "null plan");
   CU(cudaSetDevice(pl->device));
-  if (pl->persist_ok)  // one cooperative launch for all color phases of both sweeps
+  // one launch for all color phases of both sweeps (the item-pipelined
+  // dataflow kernel, else the persistent cooperative kernel)
+  if (pl->persist_ok || pl->flow2_grid > 0)
     return launch_persistent(pl, 0, r, z, nullptr, nullptr, (cudaStream_t)stream, 1);
   long long nl = 0;
   int rc = launch_forward(pl, r, pl->y, (cudaStream_t)stream, nullptr, &nl);
@@ -2365,7 +2382,7 @@ extern "C" int tb_pcg(tb_plan *pl, const double *b, double *x, double tol,
     // default whenever the TMA SpMV and the dataflow precond apply
     // (configs 2, 3, 5: 23.3 / 51.9 / 1694 ms vs 28.5 / 54.4 / ~2000 ms for
     // the single persistent launch)
-    pl->split_pcg = pl->persist_ok && pl->spmv_S > 0 &&
+    pl->split_pcg = (pl->persist_ok || pl->flow2_grid > 0) && pl->spmv_S > 0 &&
                     (se == 1 || (se < 0 && pl->n >= sn && pl->n_lvl1_flow > 0));
     // the split path runs as a CUDA graph (conditional WHILE, device-side
     // convergence test) unless TB_PCG_SPLIT_POLL=n asks for host polling

@@ -157,7 +157,7 @@ __device__ __forceinline__ void cp_async16(unsigned dst, const void *src, bool p
       : "memory");
 }
 
-template <int KC>
+template <int KC, bool LONG>
 __global__ void __launch_bounds__(kThreads)
     precond_kernel(const __grid_constant__ persist::Params P) {
   extern __shared__ __align__(128) unsigned char rsm[];
@@ -204,111 +204,166 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncwarp();
   };
-  // copies of walk step i of item (fwd, m) into ring stage st; one group
-  auto issue = [&](bool valid, bool fwd, const Meta &m, int i, int st) {
-    if (valid) {
-      const int off = __shfl_sync(full, m.off, i);
-      const int len = __shfl_sync(full, m.len, i);
-      const unsigned sb = ring_s + st * ST;
-      const char *vp = (const char *)((fwd ? P.Lval : P.Uval) + off);
-      const char *cp = (const char *)((fwd ? P.Lce : P.Uce) + off);
+  // A ring stage holds one CHUNK: up to KC slots of a step's slice (LONG:
+  // slices longer than KC take several chunks; else a step is one chunk)
+  // plus, with a step's first chunk, its inv_d row and -- forward -- rhs row.
+  auto nchunks = [&](int len) { return LONG ? (len > KC ? (len + KC - 1) / KC : 1) : 1; };
+  // copies of chunk c of walk step i of item (fwd, m) into ring stage st
+  auto copy_chunk = [&](bool fwd, const Meta &m, int i, int c, int st) {
+    const int off = __shfl_sync(full, m.off, i) + (LONG ? c * KC * 32 : 0);
+    int len = __shfl_sync(full, m.len, i);
+    if (LONG) {
+      len -= c * KC;
+      len = len > KC ? KC : len;
+    }
+    const unsigned sb = ring_s + st * ST;
+    const char *vp = (const char *)((fwd ? P.Lval : P.Uval) + off);
+    const char *cp = (const char *)((fwd ? P.Lce : P.Uce) + off);
 #pragma unroll
-      for (int r = 0; r < (KC * 16 + 31) / 32; ++r) {
-        const int c = lane + 32 * r;
-        cp_async16(sb + c * 16, vp + c * 16, c < len * 16);
-      }
+    for (int r = 0; r < (KC * 16 + 31) / 32; ++r) {
+      const int q = lane + 32 * r;
+      cp_async16(sb + q * 16, vp + q * 16, q < len * 16);
+    }
 #pragma unroll
-      for (int r = 0; r < (KC * 8 + 31) / 32; ++r) {
-        const int c = lane + 32 * r;
-        cp_async16(sb + KC * 256 + c * 16, cp + c * 16, c < len * 8);
-      }
+    for (int r = 0; r < (KC * 8 + 31) / 32; ++r) {
+      const int q = lane + 32 * r;
+      cp_async16(sb + KC * 256 + q * 16, cp + q * 16, q < len * 8);
+    }
+    if (!LONG || c == 0) {
       const size_t row0 = (size_t)m.k * span + (fwd ? i : b_s - 1 - i) * 32;
       // lanes 0-15: inv_d row; lanes 16-31: rhs row (forward: an input)
       const double *q = lane < 16 ? P.inv_d + row0 + lane * 2 : src + row0 + (lane - 16) * 2;
       cp_async16(sb + KC * 384 + lane * 16, q, lane < 16 || fwd);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  Meta cur = load_meta(gw);
-  // prologue: steps 0 .. D-2 of the first item (b_s >= D - 1)
+  Meta cur = load_meta(gw), nx;
+  nx.off = nx.len = nx.k = 0;
+  nx.dep = -1;
+  bool fwd = gw < n, fwdn = false, has_n = false;
+  // issue cursor: chunk ic of walk step is of the current (inx = false) or
+  // the next item; it runs D-1 chunks ahead of the consumer (an item has at
+  // least b_s >= D-1 chunks, so it never leaves the next item)
+  int is = 0, ic = 0, sti = 0;
+  bool inx = false;
+  auto issue_next = [&]() {
+    const bool valid = is < b_s && (!inx || has_n);
+    if (valid) {
+      const Meta &m = inx ? nx : cur;
+      copy_chunk(inx ? fwdn : fwd, m, is, ic, sti);
+      if (LONG) {
+        const int len = __shfl_sync(full, m.len, is);
+        ic = ic + 1 < nchunks(len) ? ic + 1 : 0;
+      }
+      if (ic == 0) {
+        ++is;
+        if (is == b_s && !inx) {
+          inx = true;
+          is = 0;
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    sti = sti + 1 == D ? 0 : sti + 1;
+  };
+  // prologue: the first D-1 chunks of the warp's first item
 #pragma unroll
-  for (int t = 0; t < D - 1; ++t) issue(true, gw < n, cur, t, t);
-  int st = 0;  // stage of the step about to be consumed
+  for (int t = 0; t < D - 1; ++t) {
+    if constexpr (LONG) {
+      issue_next();
+    } else {
+      copy_chunk(fwd, cur, t, 0, t);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  }
+  int st = 0;  // stage of the chunk about to be consumed
   for (int it = gw; it < total; it += NW) {
-    const bool fwd = it < n;
     const int k = cur.k;
     const int itn = it + NW;
-    const bool has_n = itn < total;
-    const bool fwdn = itn < n;
-    Meta nx;
-    nx.off = nx.len = nx.k = 0;
-    nx.dep = -1;
+    has_n = itn < total;
+    fwdn = itn < n;
     if (has_n) nx = load_meta(itn);
     wait_deps(cur);
     double *dst = fwd ? mid : out;
     double rhs_reg = 0.0;
     if (!fwd) rhs_reg = __ldcg(mid + (size_t)k * span + (b_s - 1) * 32 + lane);
     for (int i = 0; i < b_s; ++i) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
-      __syncwarp();
-      {
-        // stream step i + D - 1 (this item's or the next one's) into the
-        // stage consumed last step
-        const int t = i + D - 1;
-        const bool here = t < b_s;
-        int sn = st + D - 1;
-        sn = sn >= D ? sn - D : sn;
-        if (here)
-          issue(true, fwd, cur, t, sn);
-        else
-          issue(has_n, fwdn, nx, t - b_s, sn);
-      }
       const int len = __shfl_sync(full, cur.len, i);
       const int row = k * span + (fwd ? i : b_s - 1 - i) * 32 + lane;
-      const unsigned char *sb = wsm + st * ST;
-      const int *se = (const int *)(sb + KC * 256) + lane;
-      const double *sv = (const double *)sb + lane;
-      Buf<KC> b;
-      double x[KC];
+      const int nch = nchunks(len);
+      double y = 0.0, idg = 0.0, rhs_next = 0.0;
+      bool pad = false;
+      for (int c = 0; c < nch; ++c) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
+        __syncwarp();
+        if constexpr (LONG) {
+          issue_next();  // into the stage consumed one chunk ago
+        } else {
+          // one chunk per step: stream step i + D - 1 (this item's or the
+          // next one's) into the stage consumed last step
+          const int t = i + D - 1;
+          int sn = st + D - 1;
+          sn = sn >= D ? sn - D : sn;
+          if (t < b_s)
+            copy_chunk(fwd, cur, t, 0, sn);
+          else if (has_n)
+            copy_chunk(fwdn, nx, t - b_s, 0, sn);
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        int clen = len;
+        if (LONG) {
+          clen -= c * KC;
+          clen = clen > KC ? KC : clen;
+        }
+        const unsigned char *sb = wsm + st * ST;
+        const int *se = (const int *)(sb + KC * 256) + lane;
+        const double *sv = (const double *)sb + lane;
+        Buf<KC> b;
+        double x[KC];
 #pragma unroll
-      for (int u0 = 0; u0 < KC; u0 += 2) {
-        if (u0 == 0 || len > u0) {  // warp-uniform
+        for (int u0 = 0; u0 < KC; u0 += 2) {
+          if (u0 == 0 || clen > u0) {  // warp-uniform
 #pragma unroll
-          for (int u = u0; u < u0 + 2 && u < KC; ++u) {
-            b.e[u] = se[u * 32];
-            const char *base = b.e[u] >= 0 ? (const char *)dst : ys_base;
-            x[u] = ld_operand(base + 8ll * b.e[u], u < len);
+            for (int u = u0; u < u0 + 2 && u < KC; ++u) {
+              b.e[u] = se[u * 32];
+              const char *base = b.e[u] >= 0 ? (const char *)dst : ys_base;
+              x[u] = ld_operand(base + 8ll * b.e[u], u < clen);
+            }
           }
         }
-      }
-      double rhs_next = 0.0;
-      if (!fwd && i + 1 < b_s) rhs_next = __ldcg(mid + row - 32);
-#pragma unroll
-      for (int u0 = 0; u0 < KC; u0 += 2) {
-        if (u0 == 0 || len > u0) {
-#pragma unroll
-          for (int u = u0; u < u0 + 2 && u < KC; ++u) b.v[u] = sv[u * 32];
+        if (!LONG || c == 0) {
+          if (!fwd && i + 1 < b_s) rhs_next = __ldcg(mid + row - 32);
         }
+#pragma unroll
+        for (int u0 = 0; u0 < KC; u0 += 2) {
+          if (u0 == 0 || clen > u0) {
+#pragma unroll
+            for (int u = u0; u < u0 + 2 && u < KC; ++u) b.v[u] = sv[u * 32];
+          }
+        }
+        if (!LONG || c == 0) {
+          idg = *((const double *)(sb + KC * 384) + lane);
+          y = fwd ? *((const double *)(sb + KC * 384 + 256) + lane) : rhs_reg;
+        }
+        chain<0, KC>(clen, y, pad, b, x, pad_code);
+        st = st + 1 == D ? 0 : st + 1;
       }
-      b.idg = *((const double *)(sb + KC * 384) + lane);
-      double y = fwd ? *((const double *)(sb + KC * 384 + 256) + lane) : rhs_reg;
-      bool pad = false;
-      chain<0, KC>(len, y, pad, b, x, pad_code);
       if (pad) y = __dsub_rn(y, __dmul_rn(0.0, y));
-      y = __dmul_rn(y, b.idg);
+      y = __dmul_rn(y, idg);
       ys[i * 32] = y;
       dst[row] = y;
       rhs_reg = rhs_next;
-      st = st + 1 == D ? 0 : st + 1;
     }
     __syncwarp();
     if (lane == 0) persist::st_release(flags + (fwd ? k : n + k), epoch);
+    // the issue cursor is inside the next item by now: it becomes current
     cur = nx;
+    fwd = fwdn;
+    inx = false;
+    if (!has_n) is = b_s;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
-
 
 template <int KC>
 __host__ inline size_t smem_bytes(int b_s) {

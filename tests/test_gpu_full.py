@@ -488,11 +488,14 @@ def test_every_precond_path_bitwise(P, name, env, monkeypatch):
 
 @pytest.mark.parametrize("name,expect", [("var7_16_b8_w32", True), ("aniso12_b16_w32", True),
                                          ("lap7_12_b4_w8", False),
-                                         ("s27_10_b8_w32", False)])
+                                         ("s27_10_b8_w32", True),
+                                         ("knn3000_b4_w32", None)])
 def test_flow_kernel_selection(P, name, expect):
     """The item-pipelined dataflow kernel (csrc/flow2.cuh) runs exactly where
-    its preconditions hold: w = 32, slices of at most 8 slots, at most 32
-    dependencies per level-1 block; TB_FLOW2=0 leaves the persistent kernel."""
+    its preconditions hold: w = 32 and at most 32 dependencies per level-1
+    block (slices longer than 8 slots run it with chunked ring stages; the
+    kNN graph's long dependency lists keep the per-phase kernels);
+    TB_FLOW2=0 leaves the persistent / per-phase kernels."""
     from paper_1908_00741_b200 import solver
     try:
         a, bs, w, _ = golden_matrix(name)
