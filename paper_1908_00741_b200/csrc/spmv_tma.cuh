@@ -57,8 +57,12 @@ __device__ __forceinline__ void issue(const Params &p, long long q, unsigned cha
   const unsigned cnt = (unsigned)(b - a);
   tma::mbar_arrive_expect_tx(bar, cnt * 12u);
   if (cnt) {
-    tma::bulk_g2s(stage, p.val + a, cnt * 8u, bar);
-    tma::bulk_g2s(stage + (size_t)cap * 8, p.col + a, cnt * 4u, bar);
+    // the matrix stream is read once: evict-first, so it does not flush the
+    // gathered vector out of L2 (config 2 45.2 -> 42.5 us, config 3 582 ->
+    // 551, config 4 406 -> 366, config 5 2257 -> 2223; profiles r03h)
+    const unsigned long long pol = tma::policy_evict_first();
+    tma::bulk_g2s_hint(stage, p.val + a, cnt * 8u, bar, pol);
+    tma::bulk_g2s_hint(stage + (size_t)cap * 8, p.col + a, cnt * 4u, bar, pol);
   }
 }
 
