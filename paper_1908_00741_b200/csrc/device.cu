@@ -1716,6 +1716,20 @@ int configure_flow2(tb_plan *pl, int kc, bool long_slices, const std::vector<int
   int ps = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, flow2::kThreads, smem));
   if (ps < 1) return TB_OK;
+  {
+    // Small systems: when a color has fewer level-1 blocks than two rounds of
+    // the full grid, the items in flight overlap the blocks they depend on
+    // and warps wait on flags; 4 CTAs (16 warps) per SM is faster there
+    // (config 2: 81.9 vs 90.2 us with 5; profiles r03j).
+    long long cmin = nl;
+    for (long long c = 0; c < pl->n_c; ++c)
+      cmin = std::min(cmin, pl->color_lvl1[c + 1] - pl->color_lvl1[c]);
+    const long long warps_full = (long long)ps * pl->num_sms * (flow2::kThreads / 32);
+    if (ps > 4 && cmin < 2 * warps_full) ps = 4;
+  }
+  // the descriptor / encoding kernels above ran on the default stream: done
+  // before any launch on the plan's or a caller's (non-blocking) stream
+  CU(cudaStreamSynchronize(0));
   pl->flow2_smem = smem;
   pl->flow2_long = long_slices;
   pl->persist_kc = kc;
