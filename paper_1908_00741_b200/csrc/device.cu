@@ -1674,6 +1674,8 @@ int configure_flow2(tb_plan *pl, int kc, bool long_slices, const std::vector<int
   }
   int rc;
   if ((rc = upload(&pl->dep2, dep.data(), (long long)dep.size()))) return rc;
+  // the descriptor kernel below reads plain block indices; afterwards bit 31
+  // marks backward items whose block no later item reads (they publish no flag)
   if ((rc = upload(&pl->item_k, item_k.data(), (long long)item_k.size()))) return rc;
   CU(cudaMalloc((void **)&pl->item_meta, sizeof(int2) * (size_t)(2 * nl * b_s)));
   {
@@ -1682,6 +1684,15 @@ int configure_flow2(tb_plan *pl, int kc, bool long_slices, const std::vector<int
         pl->L.slice_ptr, pl->L.slice_len, pl->U.slice_ptr, pl->U.slice_len, pl->item_k,
         pl->item_meta, (int)nl, (int)b_s);
     CU(cudaGetLastError());
+  }
+  {
+    std::vector<char> read_by((size_t)nl, 0);
+    for (int q : bd) read_by[q] = 1;      // (bd has a dummy 0 entry only when no list has entries)
+    if (bp[nl] == 0) std::fill(read_by.begin(), read_by.end(), 0);
+    for (long long it = nl; it < 2 * nl; ++it)
+      if (!read_by[item_k[it]]) item_k[it] |= (int)0x80000000;
+    CU(cudaStreamSynchronize(0));  // build_item_meta has read the plain indices
+    CU(cudaMemcpy(pl->item_k, item_k.data(), sizeof(int) * item_k.size(), cudaMemcpyHostToDevice));
   }
   pl->dep_stride = ds;
   // encoded column arrays (in-block / padding slots pre-classified)

@@ -46,7 +46,9 @@
 // [forward flags | backward flags], fixed stride, -1 padded: a backward item
 // lists its own forward block next to the later-color blocks its U rows read.
 // Every dependency precedes its reader in the item order and each warp walks
-// its items in order, so the lowest unfinished item can always run.
+// its items in order, so the lowest unfinished item can always run.  Backward
+// items whose block no later item reads (the first color's) publish no flag
+// and skip the release fence.
 //
 // Requirements (host-checked; otherwise the plan keeps persist.cuh's kernel):
 // w == 32, kStages <= b_s <= 32, every slice <= KC <= 8 slots, <= 32
@@ -142,7 +144,8 @@ __device__ __forceinline__ void chain(int len, double &y, bool &pad, const Buf<K
 struct Meta {
   int off, len;  // lane i < b_s: walk step i's slice offset (slots) and length
   int dep;       // lane q: q-th dependency (index into the flag array) or -1
-  int k;         // the item's level-1 block
+  int k;         // the item's level-1 block; bit 31 set: no later item reads its result
+                 // (backward items of the first color): no flag to publish
 };
 
 // ---------------------------------------------------------------- kernel
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(kThreads)
       cp_async16(sb + KC * 256 + q * 16, cp + q * 16, q < len * 8, pol_stream);
     }
     if (!LONG || c == 0) {
-      const size_t row0 = (size_t)m.k * span + (fwd ? i : b_s - 1 - i) * 32;
+      const size_t row0 = (size_t)(m.k & 0x7fffffff) * span + (fwd ? i : b_s - 1 - i) * 32;
       // lanes 0-15: inv_d row; lanes 16-31: rhs row (forward: an input)
       const double *q = lane < 16 ? P.inv_d + row0 + lane * 2 : src + row0 + (lane - 16) * 2;
       cp_async16(sb + KC * 384 + lane * 16, q, lane < 16 || fwd, pol_stream);
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(kThreads)
   }
   int st = 0;  // stage of the chunk about to be consumed
   for (int it = gw; it < total; it += NW) {
-    const int k = cur.k;
+    const int k = cur.k & 0x7fffffff;
     const int itn = it + NW;
     has_n = itn < total;
     fwdn = itn < n;
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(kThreads)
       rhs_reg = rhs_next;
     }
     __syncwarp();
-    if (lane == 0) persist::st_release(flags + (fwd ? k : n + k), epoch);
+    if (lane == 0 && cur.k >= 0) persist::st_release(flags + (fwd ? k : n + k), epoch);
     // the issue cursor is inside the next item by now: it becomes current
     cur = nx;
     fwd = fwdn;
