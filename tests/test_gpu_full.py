@@ -511,6 +511,35 @@ def test_flow_kernel_selection(P, name, expect):
     st.plan.close()
 
 
+@pytest.mark.parametrize("bs", [2, 3, 5, 8, 16, 32])
+@pytest.mark.parametrize("kind", ["var7", "s27"])
+def test_flow_kernel_block_sizes(P, bs, kind):
+    """Every block size the flow kernel accepts (3 <= b_s <= 32, odd ones
+    included; b_s = 2 keeps the persistent kernel), short (7-point) and long
+    (27-point, chunked ring stages) slices: z = M r bitwise vs the oracle,
+    over repeated applications (fresh flag epochs)."""
+    import torch
+    import workloads as problems
+    from oracle import oracle as O
+    from paper_1908_00741_b200 import solver
+    a = problems.varcoef7(14, seed=2) if kind == "var7" else problems.stencil27(12, seed=2)
+    cfg = P.CgConfig(ordering="hbmc", b_s=bs, w=32, spmv_format="sell")
+    st = solver.attach_plan(solver.prepare(a, np.zeros(a.n), cfg), cfg)
+    assert (st.plan.flow_info()["grid"] > 0) == (bs >= 3)
+    ob = O.HbmcSystem(O.Csr(a.n, a.row_ptr, a.col_idx, a.vals), np.zeros(a.n), bs, 32)
+    rng = np.random.default_rng(bs)
+    for _ in range(3):
+        r = rng.standard_normal(st.layout.n_pad)
+        rt = torch.from_numpy(r).cuda()
+        z = torch.full_like(rt, float("nan"))
+        st.plan.precond(rt, z)
+        torch.cuda.synchronize()
+        yo = O.hbmc_sweep(True, ob.Ls, ob.inv_d, r, ob.hl)
+        zo = O.hbmc_sweep(False, ob.Us, ob.inv_d, yo, ob.hl)
+        assert np.array_equal(z.cpu().numpy(), zo)
+    st.plan.close()
+
+
 def test_flow_kernel_signed_zero_and_padding_rule(P):
     """Padding slots are y - 0*y in the reference (identity except -0 -> +0).
     The flow kernel applies that map once per padded row; rows of a right-hand
