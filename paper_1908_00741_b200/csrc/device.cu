@@ -1966,11 +1966,22 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
     // item-pipelined dataflow kernel: no grid barrier, so a plain launch of
     // the co-resident grid; inside the split PCG graph the epoch comes from
     // device memory like the persistent kernel's
-    if (pl->in_graph) P.epoch_dev = pl->epoch_dev;
-    flow2_fn(pl->persist_kc, pl->flow2_long)<<<pl->flow2_grid, flow2::kThreads, pl->flow2_smem,
-                                               s>>>(P);
-    if (pl->in_graph && !pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
-    CU(cudaGetLastError());
+    if (pl->in_graph) {
+      // captured into the split PCG graph: a plain launch (the graph runs its
+      // kernels one after another, so the co-resident grid is resident)
+      P.epoch_dev = pl->epoch_dev;
+      flow2_fn(pl->persist_kc, pl->flow2_long)<<<pl->flow2_grid, flow2::kThreads,
+                                                 pl->flow2_smem, s>>>(P);
+      if (!pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
+      CU(cudaGetLastError());
+      return TB_OK;
+    }
+    // stand-alone: a cooperative launch, so the whole grid is guaranteed
+    // co-resident (warps wait on flags of items other CTAs own) even when
+    // other work shares the device
+    CU(cudaLaunchCooperativeKernel((const void *)flow2_fn(pl->persist_kc, pl->flow2_long),
+                                   dim3(pl->flow2_grid), dim3(flow2::kThreads), args,
+                                   pl->flow2_smem, s));
     return TB_OK;
   }
   if (mode == 0 && P.n_lvl1 > 0 && pl->in_graph) {
