@@ -1963,25 +1963,16 @@ int launch_persistent(tb_plan *pl, int mode, const double *src, double *dst, con
   P.watchdog = (long long)env_int("TB_WATCHDOG_MS", 2000) * 1900000LL;
   void *args[] = {&P};
   if (mode == 0 && P.n_lvl1 > 0 && pl->flow2_grid > 0) {
-    // item-pipelined dataflow kernel: no grid barrier, so a plain launch of
-    // the co-resident grid; inside the split PCG graph the epoch comes from
-    // device memory like the persistent kernel's
-    if (pl->in_graph) {
-      // captured into the split PCG graph: a plain launch (the graph runs its
-      // kernels one after another, so the co-resident grid is resident)
-      P.epoch_dev = pl->epoch_dev;
-      flow2_fn(pl->persist_kc, pl->flow2_long)<<<pl->flow2_grid, flow2::kThreads,
-                                                 pl->flow2_smem, s>>>(P);
-      if (!pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
-      CU(cudaGetLastError());
-      return TB_OK;
-    }
-    // stand-alone: a cooperative launch, so the whole grid is guaranteed
-    // co-resident (warps wait on flags of items other CTAs own) even when
-    // other work shares the device
+    // Item-pipelined dataflow kernel (flow2.cuh).  A cooperative launch, stand-alone and as a node of the split PCG graph
+    // alike: the whole grid is guaranteed co-resident (warps wait on flags of
+    // items other CTAs own).  In the graph the epoch comes from device memory
+    // (bumped by the p-update kernel or a 1-thread kernel after the launch).
+    if (pl->in_graph) P.epoch_dev = pl->epoch_dev;
     CU(cudaLaunchCooperativeKernel((const void *)flow2_fn(pl->persist_kc, pl->flow2_long),
                                    dim3(pl->flow2_grid), dim3(flow2::kThreads), args,
                                    pl->flow2_smem, s));
+    if (pl->in_graph && !pl->defer_bump) epoch_bump<<<1, 1, 0, s>>>(pl->epoch_dev);
+    CU(cudaGetLastError());
     return TB_OK;
   }
   if (mode == 0 && P.n_lvl1 > 0 && pl->in_graph) {
