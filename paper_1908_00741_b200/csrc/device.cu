@@ -36,7 +36,6 @@
 using tb::fail;
 
 #include "sweep_lean.cuh"
-#include "sweep_group.cuh"
 #include "spmv_tma.cuh"
 #include "persist.cuh"
 #include "flow2.cuh"
@@ -910,15 +909,10 @@ struct tb_plan {
     int ring = 0;                  // ring depth (ring kernel)
     size_t smem = 0;
     unsigned grid = 0;
-    int kind = 0;                  // 0 simple, 4 lean, 5 group (TMA operand ring)
-    int gcap = 0, gD = 0, gA = 2;  // group kernel: stage slot capacity, stages, gather distance
-    size_t gsmem = 0;              // group kernel: dynamic shared memory, grid (0 = not sized yet)
-    unsigned ggrid = 0;
+    int kind = 0;                  // 0 simple, 4 lean
     int block = 256;               // threads per CTA (lean)
   };
   std::vector<ColorLaunch> cl_fwd, cl_bwd;
-  CUtensorMap tm_idg;           // inv_d as [block][step][lane] (group kernel)
-  bool tm_idg_ok = false, group_failed = false;
   int num_sms = 148;
   // task sweeps
   DevCsr Lc, Uc, Ac;
@@ -987,6 +981,8 @@ namespace {
 // the measured-fastest paths; the switches exist so the test suite can force
 // every path (tests/test_gpu_full.py) and for diagnostics -- none changes
 // results beyond the documented +-1 iteration / 1e-10 bar:
+//   TB_FLOW2=0          no item-pipelined dataflow kernel (flow2.cuh): the
+//                       persistent / per-phase kernels run the preconditioner
 //   TB_PERSIST=0        no persistent kernels (per-phase sweeps, graph PCG)
 //   TB_PERSIST_MIN_N=n  smallest n for the persistent barrier-mode kernel
 //   TB_DATAFLOW=0       barrier-separated color phases instead of per-block flags
@@ -1001,106 +997,10 @@ namespace {
 //   TB_L2WIN=0          no L2 persisting window over the CG vectors
 //   TB_DEBUG_SYNC=1     synchronise after every stage of a host-polled iteration
 //   TB_TRACE=1          in-kernel phase timestamps (tb_plan_trace)
+//   TB_WATCHDOG_MS=n    watchdog of the in-kernel waits (default 2000; 0 = no trap)
 int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return v && *v ? atoi(v) : dflt;
-}
-
-// ---- group kernel (sweep_group.cuh) host side
-using GroupFn = void (*)(const CUtensorMap, const CUtensorMap, const sweep_group::Params);
-
-template <bool FWD>
-GroupFn group_fn(int kc, int a) {
-#define TB_GROUP_ROW(K)                                                  \
-  case K:                                                                \
-    return a == 1 ? sweep_group::sweep_kernel<FWD, K, 1>                 \
-         : a == 3 ? sweep_group::sweep_kernel<FWD, K, 3>                 \
-                  : sweep_group::sweep_kernel<FWD, K, 2>;
-  switch (kc) {
-    TB_GROUP_ROW(2)
-    TB_GROUP_ROW(4)
-    TB_GROUP_ROW(6)
-    default:
-    TB_GROUP_ROW(8)
-  }
-#undef TB_GROUP_ROW
-}
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_tiled_fn() {
-  static EncodeTiledFn fn = [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    cudaGetLastError();
-    return (EncodeTiledFn)p;
-  }();
-  return fn;
-}
-
-// A length n_lvl1 * b_s * 32 vector as the 3-D tensor [block][step][lane];
-// box = kG blocks x 1 step x 32 lanes (the rows one job of a group reads).
-int make_vec_map(CUtensorMap *tm, const double *v, long long b_s, long long n_lvl1) {
-  EncodeTiledFn fn = encode_tiled_fn();
-  if (!fn) return fail(TB_ECUDA, "cuTensorMapEncodeTiled is not available in this driver");
-  cuuint64_t dims[3] = {32, (cuuint64_t)b_s, (cuuint64_t)n_lvl1};
-  cuuint64_t strides[2] = {256, (cuuint64_t)(256 * b_s)};
-  cuuint32_t box[3] = {32, 1, (cuuint32_t)sweep_group::kG};
-  cuuint32_t es[3] = {1, 1, 1};
-  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)v, dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return TB_OK;
-}
-
-// Size the group kernel for one color: stage capacity = the largest job
-// (slots of one step over the kG blocks of a group), as many stages as fit
-// two CTAs per SM (one if that leaves fewer than A + 2).
-int configure_group(tb_plan *pl, const tb_sell_host &h, tb_plan::ColorLaunch &L, int smem_optin) {
-  const int G = sweep_group::kG, b_s = (int)pl->b_s;
-  long long cap = 0;
-  for (long long kg0 = L.k0; kg0 < L.k1; kg0 += G) {
-    const long long gn = L.k1 - kg0 < G ? L.k1 - kg0 : G;
-    for (int l = 0; l < b_s; ++l) {
-      long long c = 0;
-      for (long long i = 0; i < gn; ++i) c += h.slice_len[(kg0 + i) * b_s + l];
-      cap = c > cap ? c : cap;
-    }
-  }
-  cap = cap * 32 < 32 ? 32 : cap * 32;
-  const int A = std::min(3, std::max(1, env_int("TB_GROUP_A", 2)));
-  const size_t fixed = sweep_group::smem_bytes((int)cap, 0, b_s);
-  const size_t sb = sweep_group::stage_bytes((int)cap);
-  int D = 0;
-  const int want = env_int("TB_GROUP_D", 0);
-  for (int per : {2, 1}) {
-    const size_t budget = ((size_t)228 * 1024 - (size_t)per * 1024) / per;
-    const size_t lim = budget < (size_t)smem_optin ? budget : (size_t)smem_optin;
-    if (lim <= fixed) continue;
-    int d = (int)((lim - fixed) / sb);
-    d = d > 8 ? 8 : d;
-    if (want > 0 && want <= d) d = want;
-    if (d >= A + 2) {
-      D = d;
-      break;
-    }
-  }
-  if (D == 0) return TB_OK;  // keep the lean kernel
-  L.kind = 5;
-  L.gcap = (int)cap;
-  L.gD = D;
-  L.gA = A;
-  L.gsmem = sweep_group::smem_bytes((int)cap, D, b_s);
-  L.ggrid = 0;  // sized at the first launch (occupancy of the FWD / BWD instantiation)
-  return TB_OK;
 }
 
 // Per color: pick the sweep kernel and size its launch.
@@ -1114,7 +1014,6 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
   out.assign(pl->n_c, tb_plan::ColorLaunch());
   const char *mode = getenv("TB_SWEEP");
   const bool force_simple = mode && !strcmp(mode, "simple");
-  const bool group_mode = mode && !strcmp(mode, "group");
   const int w = (int)pl->w, b_s = (int)pl->b_s;
   size_t smem_optin = 227 * 1024;
   int v = 0;
@@ -1147,11 +1046,6 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
       L.smem = sweep_lean::smem_bytes(b_s, L.block);
       L.grid = grid_for((L.k1 - L.k0) * w, L.block);
     }
-    if (L.kind == 4 && group_mode && w == 32 && b_s % 4 == 0 && L.max_slots <= 8 &&
-        pl->color_lvl1.back() >= sweep_group::kG) {
-      int rc = configure_group(pl, h, L, (int)smem_optin);
-      if (rc) return rc;
-    }
   }
   static bool attr_done = false;
   if (!attr_done) {
@@ -1176,52 +1070,9 @@ int configure_sweeps(tb_plan *pl, const tb_sell_host &h,
 
 // Launch the configured kernel of one color phase.
 template <bool FWD>
-int launch_group(tb_plan *pl, const tb_plan::ColorLaunch &L, const DevSell &M,
-                 const double *src, double *dst, cudaStream_t s, const PcgState *st) {
-  GroupFn fn = group_fn<FWD>(L.max_slots, L.gA);
-  const long long n_lvl1 = pl->color_lvl1.back();
-  unsigned &grid = const_cast<tb_plan::ColorLaunch &>(L).ggrid;
-  if (grid == 0) {
-    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    int per_sm = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, sweep_group::kThreads, L.gsmem));
-    if (per_sm < 1) return fail(TB_ECUDA, "group sweep kernel does not fit an SM");
-    const long long ng = (L.k1 - L.k0 + sweep_group::kG - 1) / sweep_group::kG;
-    const long long g = (long long)per_sm * pl->num_sms;
-    grid = (unsigned)(ng < g ? ng : g);
-  }
-  if (!pl->tm_idg_ok) {
-    int rc = make_vec_map(&pl->tm_idg, pl->inv_d, pl->b_s, n_lvl1);
-    if (rc) return rc;
-    pl->tm_idg_ok = true;
-  }
-  CUtensorMap tm_rhs;
-  int rc = make_vec_map(&tm_rhs, src, pl->b_s, n_lvl1);
-  if (rc) return rc;
-  sweep_group::Params P;
-  P.slice_ptr = M.slice_ptr;
-  P.slice_len = M.slice_len;
-  P.col = M.col;
-  P.val = M.val;
-  P.dst = dst;
-  P.b_s = (int)pl->b_s;
-  P.k0 = (int)L.k0;
-  P.k1 = (int)L.k1;
-  P.cap = L.gcap;
-  P.D = L.gD;
-  P.done = st ? &st->done : nullptr;
-  fn<<<grid, sweep_group::kThreads, L.gsmem, s>>>(tm_rhs, pl->tm_idg, P);
-  return TB_OK;
-}
-
-template <bool FWD>
 void launch_phase(tb_plan *pl, const tb_plan::ColorLaunch &L, const DevSell &M,
                   const double *src, double *dst, cudaStream_t s, const PcgState *st) {
-  if (L.kind == 5 && ((uintptr_t)src & 15) == 0) {
-    if (launch_group<FWD>(pl, L, M, src, dst, s, st)) pl->group_failed = true;
-    return;
-  }
-  if (L.kind == 4 || L.kind == 5) {
+  if (L.kind == 4) {
     const long long nt = (L.k1 - L.k0) * pl->w;
     const bool w32 = pl->w == 32;
     auto fn = L.max_slots == 2 ? (w32 ? sweep_lean::sweep_kernel<FWD, 2, 32> : sweep_lean::sweep_kernel<FWD, 2, 0>)
@@ -1253,7 +1104,6 @@ int launch_forward(tb_plan *pl, const double *src, double *dst, cudaStream_t s,
       launch_phase<true>(pl, pl->cl_fwd[c], pl->L, src, dst, s, st);
       ++*nl;
     }
-    if (pl->group_failed) return TB_ECUDA;
   } else {
     for (long long ph = 0; ph < pl->fs.n_phases; ++ph) {
       const long long t0 = pl->fs.phase_ptr[ph], t1 = pl->fs.phase_ptr[ph + 1];
@@ -1278,7 +1128,6 @@ int launch_backward(tb_plan *pl, const double *src, double *dst, cudaStream_t s,
       launch_phase<false>(pl, pl->cl_bwd[c], pl->U, src, dst, s, st);
       ++*nl;
     }
-    if (pl->group_failed) return TB_ECUDA;
   } else {
     for (long long ph = pl->bs.n_phases - 1; ph >= 0; --ph) {
       const long long t0 = pl->bs.phase_ptr[ph], t1 = pl->bs.phase_ptr[ph + 1];
