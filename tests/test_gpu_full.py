@@ -576,7 +576,7 @@ def test_flow_kernel_signed_zero_and_padding_rule(P):
 
 
 @pytest.mark.parametrize("name", ["knn3000_b4_w32", "aniso12_b16_w32", "lap7_12_b4_w8"])
-@pytest.mark.parametrize("env", [{}, {"TB_PCG_SPLIT": "0"}, {"TB_PCG_SPLIT_POLL": "2"},
+@pytest.mark.parametrize("env", [{}, {"TB_FLOW2": "0"}, {"TB_PCG_SPLIT": "0"}, {"TB_PCG_SPLIT_POLL": "2"},
                                  {"TB_PERSIST": "0"}, {"TB_PCG_NOGRAPH": "3"},
                                  {"TB_RZP_FUSE": "0"}, {"TB_VEC_PAIRS": "0"},
                                  {"TB_SPMV_TMA": "0"}])
