@@ -165,6 +165,25 @@ __device__ __forceinline__ void cp_async16(unsigned dst, const void *src, bool p
       "l"(src), "r"((int)pred), "l"(pol)
       : "memory");
 }
+// the same at a compile-time byte offset from both addresses (one address
+// computation per slice instead of one per 512-byte round)
+template <int OFF>
+__device__ __forceinline__ void cp_async16_at(unsigned dst, const void *src, bool pred,
+                                              unsigned long long pol) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+      " @q cp.async.cg.shared.global.L2::cache_hint [%0+%4], [%1+%4], 16, %3;\n}" ::"r"(dst),
+      "l"(src), "r"((int)pred), "l"(pol), "n"(OFF)
+      : "memory");
+}
+template <int R, int NR>
+__device__ __forceinline__ void cp_rounds(unsigned dst, const char *src, int lane, int nchunk,
+                                          unsigned long long pol) {
+  if constexpr (R < NR) {
+    cp_async16_at<R * 512>(dst, src, lane + 32 * R < nchunk, pol);
+    cp_rounds<R + 1, NR>(dst, src, lane, nchunk, pol);
+  }
+}
 __device__ __forceinline__ void st_result(double *p, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
@@ -237,16 +256,11 @@ __global__ void __launch_bounds__(kThreads)
     const unsigned sb = ring_s + st * ST;
     const char *vp = (const char *)((fwd ? P.Lval : P.Uval) + off);
     const char *cp = (const char *)((fwd ? P.Lce : P.Uce) + off);
-#pragma unroll
-    for (int r = 0; r < (KC * 16 + 31) / 32; ++r) {
-      const int q = lane + 32 * r;
-      cp_async16(sb + q * 16, vp + q * 16, q < len * 16, pol_stream);
-    }
-#pragma unroll
-    for (int r = 0; r < (KC * 8 + 31) / 32; ++r) {
-      const int q = lane + 32 * r;
-      cp_async16(sb + KC * 256 + q * 16, cp + q * 16, q < len * 8, pol_stream);
-    }
+    // 16-byte chunk lane + 32 r of the slice's values (16 per slot) and
+    // columns (8 per slot)
+    cp_rounds<0, (KC * 16 + 31) / 32>(sb + lane * 16, vp + lane * 16, lane, len * 16, pol_stream);
+    cp_rounds<0, (KC * 8 + 31) / 32>(sb + KC * 256 + lane * 16, cp + lane * 16, lane, len * 8,
+                                     pol_stream);
     if (!LONG || c == 0) {
       const size_t row0 = (size_t)(m.k & 0x7fffffff) * span + (fwd ? i : b_s - 1 - i) * 32;
       // lanes 0-15: inv_d row; lanes 16-31: rhs row (forward: an input)
