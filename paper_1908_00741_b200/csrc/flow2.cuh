@@ -262,9 +262,10 @@ __global__ void __launch_bounds__(kThreads)
     cp_rounds<0, (KC * 8 + 31) / 32>(sb + KC * 256 + lane * 16, cp + lane * 16, lane, len * 8,
                                      pol_stream);
     if (!LONG || c == 0) {
-      const size_t row0 = (size_t)(m.k & 0x7fffffff) * span + (fwd ? i : b_s - 1 - i) * 32;
-      // lanes 0-15: inv_d row; lanes 16-31: rhs row (forward: an input)
-      const double *q = lane < 16 ? P.inv_d + row0 + lane * 2 : src + row0 + (lane - 16) * 2;
+      // lanes 0-15: inv_d row; lanes 16-31: rhs row (forward: an input);
+      // 32-bit row index (n_pad < 2^31)
+      const int r0 = (m.k & 0x7fffffff) * span + (fwd ? i : b_s - 1 - i) * 32 + (lane & 15) * 2;
+      const double *q = (lane < 16 ? P.inv_d : src) + r0;
       cp_async16(sb + KC * 384 + lane * 16, q, lane < 16 || fwd, pol_stream);
     }
   };
