@@ -320,7 +320,11 @@ __global__ void __launch_bounds__(kThreads)
     double *dst = fwd ? mid : out;
     double rhs_reg = 0.0;
     if (!fwd) rhs_reg = __ldcg(mid + (size_t)k * span + (b_s - 1) * 32 + lane);
-    for (int i = 0; i < b_s; ++i) {
+    // one walk step; NEXT: its ring copies belong to the next item (the last
+    // D-1 steps of an item, one-chunk steps) -- known at compile time so the
+    // common case carries no per-step source selection
+    auto run_step = [&](int i, auto next_tag) {
+      constexpr bool NEXT = decltype(next_tag)::value;
       const int len = __shfl_sync(full, cur.len, i);
       const int row = k * span + (fwd ? i : b_s - 1 - i) * 32 + lane;
       const int nch = nchunks(len);
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(kThreads)
           const int t = i + D - 1;
           int sn = st + D - 1;
           sn = sn >= D ? sn - D : sn;
-          if (t < b_s)
+          if constexpr (!NEXT)
             copy_chunk(fwd, cur, t, 0, sn);
           else if (has_n)
             copy_chunk(fwdn, nx, t - b_s, 0, sn);
@@ -386,6 +390,13 @@ __global__ void __launch_bounds__(kThreads)
       ys[i * 32] = y;
       st_result(dst + row, y, pol_result);
       rhs_reg = rhs_next;
+    };
+    if constexpr (LONG) {
+      for (int i = 0; i < b_s; ++i) run_step(i, std::false_type{});
+    } else {
+      int i = 0;
+      for (; i < b_s - (D - 1); ++i) run_step(i, std::false_type{});
+      for (; i < b_s; ++i) run_step(i, std::true_type{});
     }
     __syncwarp();
     if (lane == 0 && cur.k >= 0) persist::st_release(flags + (fwd ? k : n + k), epoch);
