@@ -2084,6 +2084,9 @@ extern "C" int tb_plan_device_bytes(const tb_plan *pl, int64_t *bytes) {
   auto cb = [](const DevCsr &c) { return (c.n + 1) * 8 + c.nnz * 12; };
   long long b = sb(pl->L) + sb(pl->U) + sb(pl->A) + cb(pl->Lc) + cb(pl->Uc) +
                 cb(pl->Ac) + pl->n * 8 * 6 + kMaxPartials * 8;
+  if (pl->flow2_grid > 0)  // flow kernel: encoded columns, item descriptors, dependency lists
+    b += (pl->L.slots + pl->U.slots) * 4 + 2 * pl->n_lvl1_flow * (pl->b_s * 8 + 4 + pl->dep_stride * 4);
+  if (pl->n_lvl1_flow > 0) b += 2 * pl->n_lvl1_flow * 4;  // completion flags
   *bytes = b;
   return TB_OK;
 }
