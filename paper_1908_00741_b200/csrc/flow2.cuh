@@ -15,7 +15,7 @@
 //     -- its rhs row), across item boundaries, and consumes the oldest stage
 //     with short shared-memory loads.  The copies hold no registers, so D-1
 //     steps of the stream are in flight per warp (register ping-pong buffers
-//     hold one), and ~20 warps fit per SM;
+//     hold one), and 16 warps (4 CTAs) run per SM;
 //   * pre-classified columns.  The plan keeps an encoded copy of the L / U
 //     column arrays (encode_cols): a cross-block column stays the row index
 //     (>= 0), an in-block column becomes the shared-memory slot of the walk
@@ -50,12 +50,16 @@
 // items whose block no later item reads (the first color's) publish no flag
 // and skip the release fence.
 //
-// Requirements (host-checked; otherwise the plan keeps persist.cuh's kernel):
-// w == 32, kStages <= b_s <= 32, every slice <= KC <= 8 slots, <= 32
+// Requirements (host-checked; otherwise the plan keeps persist.cuh's kernel
+// or the per-phase kernels): w == 32, kStages <= b_s <= 32, <= 32
 // dependencies per item, in-block entries only inside a lane's own level-2
-// block.  What was tried and rejected on the way (profiles/README.md r02q-x):
-// register ping-pong buffers, L2 prefetch (bulk and per line), 3-4 CTAs/SM
-// with spills, gathers issued one step ahead, lazy flag publication.
+// block.  Slices of up to 8 slots run the one-chunk-per-step instantiation
+// (KC = 2 / 4 / 6 / 8), longer ones (27-point rows) the LONG one: a step is
+// several 8-slot ring chunks.  What was tried and rejected on the way
+// (profiles/README.md r02q-r03x): register ping-pong buffers, L2 prefetch of
+// the stream (bulk and per line) and of the gathered operands, 3-4 CTAs/SM
+// with spills, gathers issued one step ahead, lazy flag publication, a
+// wavefront item order, dependency lists beyond 32 entries (kNN).
 
 #pragma once
 
